@@ -1,0 +1,67 @@
+// RAII device allocation used by the host engine.
+#pragma once
+
+#include <cstddef>
+#include <utility>
+
+#include <cuda_runtime.h>
+
+#include "errors.hpp"
+
+namespace mtg {
+
+template <typename T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t n) { resize(n); }
+  ~DeviceBuffer() { release(); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+
+  // Reallocates (zero-filled) when n differs from the current size.
+  void resize(size_t n) {
+    if (n == n_ && p_) return;
+    release();
+    if (n) {
+      MTG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+      MTG_CUDA(cudaMemset(p_, 0, n * sizeof(T)));
+    }
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  void upload(const T* host, size_t n, size_t offset = 0) {
+    MTG_CUDA(cudaMemcpy(p_ + offset, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void download(T* host, size_t n, size_t offset = 0) const {
+    MTG_CUDA(cudaMemcpy(host, p_ + offset, n * sizeof(T), cudaMemcpyDeviceToHost));
+  }
+
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+}  // namespace mtg

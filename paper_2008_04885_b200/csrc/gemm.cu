@@ -1,0 +1,120 @@
+// Host side of the tcgen05 GEMM: TMA tensor maps, tile-size choice, launch.
+#include "gemm.hpp"
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "errors.hpp"
+
+namespace mtg {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    MTG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      fail(kCudaError, "cuTensorMapEncodeTiled entry point unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+CUtensorMap make_map(const void* ptr, int prec, int rows, int k_pad, int box_rows) {
+  CUtensorMap m;
+  const int elem = prec_elem_bytes(prec);
+  CUtensorMapDataType dt = prec == kPrecI8     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                           : prec == kPrecBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k_pad), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(k_pad) * elem};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem),
+                       static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(kCudaError, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+template <int PREC, int BN>
+void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  constexpr int smem = gemm_smem_bytes(PREC, BN);
+  static bool configured = false;
+  if (!configured) {
+    MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  dim3 grid(p.n_tiles, p.m_tiles);
+  gemm_tc_kernel<PREC, BN><<<grid, kGemmThreads, smem, stream>>>(p.a, p.b, p.a2, p.b2,
+                                                                 p.num_kb, ep);
+  MTG_CUDA(cudaGetLastError());
+}
+
+template <int PREC>
+void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  switch (p.bn) {
+    case 32: return launch_one<PREC, 32>(p, ep, stream);
+    case 64: return launch_one<PREC, 64>(p, ep, stream);
+    case 128: return launch_one<PREC, 128>(p, ep, stream);
+    case 256: return launch_one<PREC, 256>(p, ep, stream);
+  }
+  fail(kStateError, "gemm: unsupported tile width");
+}
+
+}  // namespace
+
+GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn) {
+  if (a.prec != b.prec || a.k_pad != b.k_pad)
+    fail(kShapeError, "gemm: operand precision / K mismatch");
+  if (a.k_pad % (128 / prec_elem_bytes(a.prec)) != 0)
+    fail(kShapeError, "gemm: K not padded to a 128-byte slab");
+  GemmPlan p;
+  p.prec = a.prec;
+  p.num_kb = a.k_pad * prec_elem_bytes(a.prec) / 128;
+  p.m_tiles = (m_max + 127) / 128;
+  int bn = force_bn;
+  if (!bn) {
+    bn = 32;
+    for (int cand : {256, 128, 64}) {
+      if (p.m_tiles * ((n + cand - 1) / cand) >= 148) {
+        bn = cand;
+        break;
+      }
+    }
+  }
+  p.bn = bn;
+  p.n_tiles = (n + bn - 1) / bn;
+  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
+  p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, bn);
+  if (a.prec == kPrecTF32x3) {
+    if (!a.ptr_lo || !b.ptr_lo) fail(kStateError, "gemm: TF32x3 needs lo operands");
+    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 128);
+    p.b2 = make_map(b.ptr_lo, b.prec, b.rows, b.k_pad, bn);
+  } else {
+    p.a2 = p.a;
+    p.b2 = p.b;
+  }
+  return p;
+}
+
+void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  switch (p.prec) {
+    case kPrecI8: return launch_prec<kPrecI8>(p, ep, stream);
+    case kPrecBF16: return launch_prec<kPrecBF16>(p, ep, stream);
+    case kPrecTF32x3: return launch_prec<kPrecTF32x3>(p, ep, stream);
+  }
+  fail(kStateError, "gemm: unknown precision");
+}
+
+}  // namespace mtg

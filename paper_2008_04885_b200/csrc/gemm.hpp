@@ -1,0 +1,42 @@
+// Host-side planning/launch of the tcgen05 GEMM (gemm_tc.cuh).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "gemm_tc.cuh"
+
+namespace mtg {
+
+// Pads K so every operand row is a whole number of 128-byte TMA/UMMA slabs.
+inline int pad_k(int k, int prec) {
+  const int per = 128 / prec_elem_bytes(prec);
+  return k <= 0 ? per : (k + per - 1) / per * per;
+}
+
+// A K-major device matrix [rows x k_pad] in the precision's operand format
+// (int8, bf16, or fp32 hi with a separate fp32 lo part for TF32x3).
+struct Operand {
+  const void* ptr = nullptr;
+  const void* ptr_lo = nullptr;  // TF32x3 only
+  int rows = 0;                  // allocated rows (TMA bound)
+  int k_pad = 0;
+  int prec = kPrecI8;
+};
+
+struct GemmPlan {
+  CUtensorMap a, b, a2, b2;
+  int prec = 0;
+  int bn = 0;
+  int num_kb = 0;
+  int m_tiles = 0;
+  int n_tiles = 0;
+};
+
+// Plans C[M x N] = A[M x K] . B[N x K]^T for at most m_max rows of A.
+GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n,
+                   int force_bn = 0);
+void launch_gemm(const GemmPlan& plan, const GemmEpilogue& ep, cudaStream_t stream);
+
+}  // namespace mtg
