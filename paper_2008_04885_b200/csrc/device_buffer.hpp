@@ -55,6 +55,17 @@ class DeviceBuffer {
     MTG_CUDA(cudaMemcpy(host, p_ + offset, n * sizeof(T), cudaMemcpyDeviceToHost));
   }
 
+  // Stream-ordered copies (the engine's stream is non-blocking, so plain
+  // cudaMemcpy would not be ordered with its kernels).
+  void upload(const T* host, size_t n, cudaStream_t st, size_t offset = 0) {
+    if (n) MTG_CUDA(cudaMemcpyAsync(p_ + offset, host, n * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  void download(T* host, size_t n, cudaStream_t st, size_t offset = 0) const {
+    if (!n) return;
+    MTG_CUDA(cudaMemcpyAsync(host, p_ + offset, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+    MTG_CUDA(cudaStreamSynchronize(st));
+  }
+
   T* get() const { return p_; }
   size_t size() const { return n_; }
   size_t bytes() const { return n_ * sizeof(T); }

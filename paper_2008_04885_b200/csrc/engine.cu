@@ -1,0 +1,689 @@
+// Device engine: weight layout, workspace, batched encoder (model.cpp:539-612)
+// and the device-resident beam-search loop (decode.cpp:34-109).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <tuple>
+
+#include "errors.hpp"
+#include "prep.cuh"
+
+namespace mtg {
+
+namespace {
+
+int gemm_prec_of(int prec) {
+  return prec == kINT8 ? kPrecI8 : prec == kBF16 ? kPrecBF16 : kPrecTF32x3;
+}
+
+int round4(int v) { return (v + 3) / 4 * 4; }
+
+// Converts fp32 K-major rows (host, [n x k]) into the operand format.
+void upload_f32_operand(const std::vector<float>& kmaj, int n, int k, int prec, DevLinear& L,
+                        cudaStream_t st) {
+  DeviceBuffer<float> tmp(std::max<size_t>(1, size_t(n) * k));
+  tmp.upload(kmaj.data(), kmaj.size());
+  if (prec == kBF16) {
+    L.h.resize(size_t(n) * L.k_pad);
+    launch_cast_bf16(tmp.get(), k, k, n, nullptr, L.h.get(), L.k_pad, st);
+  } else {
+    L.hi.resize(size_t(n) * L.k_pad);
+    L.lo.resize(size_t(n) * L.k_pad);
+    launch_split_tf32(tmp.get(), k, k, n, nullptr, L.hi.get(), L.lo.get(), L.k_pad, st);
+  }
+  MTG_CUDA(cudaStreamSynchronize(st));
+}
+
+// Builds a [N x K] K-major weight from reference tensors. `nt`: tensors are
+// already [rows = N x cols = K] (tgt_embed); otherwise [K x N] (y = x.W).
+void build_linear(DevLinear& L, const std::vector<const HostTensor*>& parts, bool nt, int prec,
+                  cudaStream_t st) {
+  const int k = static_cast<int>(nt ? parts[0]->cols() : parts[0]->rows());
+  int n = 0;
+  for (auto* p : parts) n += static_cast<int>(nt ? p->rows() : p->cols());
+  L.n = n;
+  L.k = k;
+  L.prec = gemm_prec_of(prec);
+  L.k_pad = pad_k(k, L.prec);
+  if (prec == kINT8) {
+    std::vector<int8_t> buf(size_t(n) * L.k_pad, 0);
+    std::vector<float> cs(n);
+    int n0 = 0;
+    for (auto* p : parts) {
+      if (!p->is_int8) fail(kStateError, "no quantized copy of a weight");
+      const int pn = static_cast<int>(nt ? p->rows() : p->cols());
+      for (int j = 0; j < pn; ++j) {
+        cs[n0 + j] = p->scale;
+        int8_t* dst = buf.data() + size_t(n0 + j) * L.k_pad;
+        if (nt)
+          std::copy(p->q.begin() + size_t(j) * k, p->q.begin() + size_t(j + 1) * k, dst);
+        else
+          for (int kk = 0; kk < k; ++kk) dst[kk] = p->q[size_t(kk) * pn + j];
+      }
+      n0 += pn;
+    }
+    L.q.resize(buf.size());
+    L.q.upload(buf.data(), buf.size());
+    L.col_scale.resize(n);
+    L.col_scale.upload(cs.data(), n);
+  } else {
+    std::vector<float> kmaj(size_t(n) * k);
+    int n0 = 0;
+    for (auto* p : parts) {
+      if (p->f32.empty()) fail(kStateError, "no f32 copy of a weight");
+      const int pn = static_cast<int>(nt ? p->rows() : p->cols());
+      for (int j = 0; j < pn; ++j) {
+        float* dst = kmaj.data() + size_t(n0 + j) * k;
+        if (nt)
+          std::copy(p->f32.begin() + size_t(j) * k, p->f32.begin() + size_t(j + 1) * k, dst);
+        else
+          for (int kk = 0; kk < k; ++kk) dst[kk] = p->f32[size_t(kk) * pn + j];
+      }
+      n0 += pn;
+    }
+    upload_f32_operand(kmaj, n, k, prec, L, st);
+  }
+}
+
+void upload_vec(DeviceBuffer<float>& dst, const HostTensor& t) {
+  dst.resize(t.f32.size());
+  dst.upload(t.f32.data(), t.f32.size());
+}
+
+struct PlanKey {
+  const void* a;
+  const void* b;
+  int m;
+  bool operator<(const PlanKey& o) const { return std::tie(a, b, m) < std::tie(o.a, o.b, o.m); }
+};
+
+}  // namespace
+
+Operand DevLinear::op() const {
+  if (prec == kPrecI8) return Operand{q.get(), nullptr, n, k_pad, prec};
+  if (prec == kPrecBF16) return Operand{h.get(), nullptr, n, k_pad, prec};
+  return Operand{hi.get(), lo.get(), n, k_pad, prec};
+}
+
+void ActOperand::allocate(int rows_, int k_, int prec_) {
+  rows = rows_;
+  k = k_;
+  prec = prec_;
+  k_pad = pad_k(k, prec);
+  const size_t n = size_t(rows) * k_pad;
+  if (prec == kPrecI8) {
+    q.resize(n);
+    row_scale.resize(rows);
+  } else if (prec == kPrecBF16) {
+    h.resize(n);
+  } else {
+    hi.resize(n);
+    lo.resize(n);
+  }
+}
+
+Operand ActOperand::op() const {
+  if (prec == kPrecI8) return Operand{q.get(), nullptr, rows, k_pad, prec};
+  if (prec == kPrecBF16) return Operand{h.get(), nullptr, rows, k_pad, prec};
+  return Operand{hi.get(), lo.get(), rows, k_pad, prec};
+}
+
+// ============================================================================
+// construction / weights
+// ============================================================================
+
+static std::map<PlanKey, GemmPlan>& plan_cache(const void* engine) {
+  static std::map<const void*, std::map<PlanKey, GemmPlan>> caches;
+  return caches[engine];
+}
+
+Engine::Engine(HostModel model, int precision, int device)
+    : host_(std::move(model)), prec_(precision), device_(device) {
+  if (prec_ != kF32 && prec_ != kBF16 && prec_ != kINT8)
+    fail(kUsageError, "unknown precision " + std::to_string(prec_));
+  if (host_.quantized && prec_ != kINT8) prec_ = kINT8;  // tools/minimt.cpp:317-320
+  if (prec_ == kINT8 && !host_.quantized) quantize_weights(host_);
+  const ModelConfig& c = host_.config;
+  c.validate();
+  if (!c.factor_configs.empty())
+    fail(kUsageError, "source factors are not supported by the GPU path yet");
+  int ndev = 0;
+  MTG_CUDA(cudaGetDeviceCount(&ndev));
+  if (device_ < 0 || device_ >= ndev) fail(kUsageError, "bad device id " + std::to_string(device_));
+  MTG_CUDA(cudaSetDevice(device_));
+  MTG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  MTG_CUDA(cudaMallocHost(&h_pinned_, 16 * sizeof(int)));
+  d_ = c.d_model;
+  dff_ = c.d_ff;
+  V_ = c.tgt_vocab_size;
+  Vp_ = round4(V_);
+  T_ = c.max_seq_len;
+  heads_ = c.num_heads;
+  upload_weights();
+}
+
+Engine::~Engine() {
+  cudaSetDevice(device_);
+  plan_cache(this).clear();
+  if (h_pinned_) cudaFreeHost(h_pinned_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::upload_weights() {
+  const ModelConfig& c = host_.config;
+  auto P = [&](const std::string& n) -> const HostTensor& { return host_.at(n); };
+  upload_vec(src_embed_, P("src_embed"));
+  std::vector<float> pe = make_pos_enc(c.max_seq_len, c.d_model);
+  pe_.resize(pe.size());
+  pe_.upload(pe.data(), pe.size(), stream_);
+  const HostTensor& te = P("tgt_embed");
+  if (prec_ == kINT8) {
+    tgt_embed_q_.resize(te.q.size());
+    tgt_embed_q_.upload(te.q.data(), te.q.size(), stream_);
+    tgt_scale_ = te.scale;
+  } else {
+    upload_vec(tgt_embed_f32_, te);
+  }
+  build_linear(logits_w_, {&te}, true, prec_, stream_);
+  auto ln = [&](LN& l, const std::string& p) {
+    upload_vec(l.g, P(p + ".gain"));
+    upload_vec(l.b, P(p + ".bias"));
+  };
+  enc_.clear();
+  enc_.resize(c.num_encoder_layers);
+  for (int l = 0; l < c.num_encoder_layers; ++l) {
+    const std::string p = "enc" + std::to_string(l);
+    EncLayer& L = enc_[l];
+    ln(L.n1, p + ".norm1");
+    ln(L.n2, p + ".norm2");
+    build_linear(L.qkv, {&P(p + ".attn.wq"), &P(p + ".attn.wk"), &P(p + ".attn.wv")}, false, prec_,
+                 stream_);
+    build_linear(L.wo, {&P(p + ".attn.wo")}, false, prec_, stream_);
+    build_linear(L.w1, {&P(p + ".ffn.w1")}, false, prec_, stream_);
+    build_linear(L.w2, {&P(p + ".ffn.w2")}, false, prec_, stream_);
+    upload_vec(L.b1, P(p + ".ffn.b1"));
+    upload_vec(L.b2, P(p + ".ffn.b2"));
+  }
+  if (c.num_encoder_layers > 0) ln(enc_final_, "enc_final");
+  dec_.clear();
+  dec_.resize(c.num_decoder_layers);
+  for (int l = 0; l < c.num_decoder_layers; ++l) {
+    const std::string p = "dec" + std::to_string(l);
+    DecLayer& L = dec_[l];
+    ln(L.n1, p + ".norm1");
+    ln(L.n2, p + ".norm2");
+    ln(L.n3, p + ".norm3");
+    build_linear(L.self_qkv, {&P(p + ".self.wq"), &P(p + ".self.wk"), &P(p + ".self.wv")}, false,
+                 prec_, stream_);
+    build_linear(L.self_wo, {&P(p + ".self.wo")}, false, prec_, stream_);
+    build_linear(L.cross_q, {&P(p + ".cross.wq")}, false, prec_, stream_);
+    build_linear(L.cross_kv, {&P(p + ".cross.wk"), &P(p + ".cross.wv")}, false, prec_, stream_);
+    build_linear(L.cross_wo, {&P(p + ".cross.wo")}, false, prec_, stream_);
+    build_linear(L.w1, {&P(p + ".ffn.w1")}, false, prec_, stream_);
+    build_linear(L.w2, {&P(p + ".ffn.w2")}, false, prec_, stream_);
+    upload_vec(L.b1, P(p + ".ffn.b1"));
+    upload_vec(L.b2, P(p + ".ffn.b2"));
+  }
+  ln(dec_final_, "dec_final");
+  MTG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// ============================================================================
+// workspace
+// ============================================================================
+
+void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
+  n_sent = std::max(n_sent, 1);
+  m_enc = std::max(m_enc, 1);
+  beam = std::max(beam, 1);
+  if (n_sent <= cap_sent_ && m_enc <= cap_enc_ && beam <= cap_beam_) return;
+  cap_sent_ = std::max(n_sent, cap_sent_);
+  cap_enc_ = std::max(m_enc, cap_enc_);
+  cap_beam_ = std::max(beam, cap_beam_);
+  plan_cache(this).clear();
+  const ModelConfig& c = host_.config;
+  const int N = cap_sent_, M = cap_enc_, B = cap_beam_;
+  r_max_ = N * B;
+  act_rows_ = std::max(M, r_max_);
+  const int gp = gemm_prec_of(prec_);
+  act_d_.allocate(act_rows_, d_, gp);
+  act_ff_.allocate(act_rows_, dff_, gp);
+  const size_t d = d_, dff = dff_;
+  enc_x_.resize(M * d);
+  enc_a_.resize(M * d);
+  enc_qkv_.resize(M * 3 * d);
+  enc_ctx_.resize(M * d);
+  ffh_.resize(size_t(act_rows_) * dff);
+  ckv_.clear();
+  ckv_.resize(c.num_decoder_layers);
+  for (auto& b : ckv_) b.resize(M * 2 * d);
+  dec_y_.resize(r_max_ * d);
+  dec_a_.resize(r_max_ * d);
+  dec_ctx_.resize(r_max_ * d);
+  dec_cq_.resize(r_max_ * d);
+  logits_.resize(size_t(r_max_) * Vp_);
+  qkv_cache_.clear();
+  qkv_cache_.resize(c.num_decoder_layers);
+  for (auto& b : qkv_cache_) b.resize(size_t(T_) * r_max_ * 3 * d);
+  src_ids_.resize(M);
+  src_pos_.resize(M);
+  src_off_.resize(N + 1);
+  enc_off_.resize(N);
+  enc_len_.resize(N);
+  nonfinite_.resize(1);
+  const size_t RT = size_t(r_max_) * T_;
+  step_.resize(1);
+  n_rows_.resize(1);
+  row_sent_.resize(r_max_);
+  row_prev_.resize(r_max_);
+  row_parent_.resize(r_max_);
+  row_lp_.resize(r_max_);
+  anc0_.resize(RT);
+  anc1_.resize(RT);
+  tok0_.resize(RT);
+  tok1_.resize(RT);
+  cand_tok_.resize(size_t(r_max_) * B);
+  cand_score_.resize(size_t(r_max_) * B);
+  sent_row0_.resize(N);
+  sent_live_.resize(N);
+  sent_maxlen_.resize(N);
+  sent_done_.resize(N);
+  best_has_.resize(N);
+  best_len_.resize(N);
+  best_norm_.resize(N);
+  best_lp_.resize(N);
+  best_tok_.resize(size_t(N) * T_);
+  res_len_.resize(N);
+  res_status_.resize(N);
+  res_lp_.resize(N);
+  res_norm_.resize(N);
+  res_flags_.resize(N);
+  res_tok_.resize(size_t(N) * T_);
+  sel_parent_.resize(size_t(N) * B);
+  sel_tok_.resize(size_t(N) * B);
+  sel_lp_.resize(size_t(N) * B);
+
+  BeamDev& b = beam_;
+  b.step = step_.get();
+  b.n_rows = n_rows_.get();
+  b.row_sent = row_sent_.get();
+  b.row_lp = row_lp_.get();
+  b.row_prev = row_prev_.get();
+  b.row_parent = row_parent_.get();
+  b.anc[0] = anc0_.get();
+  b.anc[1] = anc1_.get();
+  b.tok[0] = tok0_.get();
+  b.tok[1] = tok1_.get();
+  b.cand_score = cand_score_.get();
+  b.cand_tok = cand_tok_.get();
+  b.sent_row0 = sent_row0_.get();
+  b.sent_live = sent_live_.get();
+  b.sent_maxlen = sent_maxlen_.get();
+  b.sent_done = sent_done_.get();
+  b.best_has = best_has_.get();
+  b.best_norm = best_norm_.get();
+  b.best_lp = best_lp_.get();
+  b.best_len = best_len_.get();
+  b.best_tok = best_tok_.get();
+  b.res_len = res_len_.get();
+  b.res_lp = res_lp_.get();
+  b.res_norm = res_norm_.get();
+  b.res_flags = res_flags_.get();
+  b.res_status = res_status_.get();
+  b.res_tok = res_tok_.get();
+  b.sel_parent = sel_parent_.get();
+  b.sel_tok = sel_tok_.get();
+  b.sel_lp = sel_lp_.get();
+  b.N = N;
+  b.B = B;
+  b.T = T_;
+  b.R_max = r_max_;
+  b.V = V_;
+  b.alpha = 1.0f;
+  b.max_seq_len = c.max_seq_len;
+}
+
+// ============================================================================
+// building blocks
+// ============================================================================
+
+void Engine::prep(const float* x, long long ldx, int k, int max_rows, const int* d_rows,
+                  const int* seg_off, int n_seg, ActOperand& out) {
+  if (prec_ == kINT8) {
+    if (seg_off)
+      launch_quantize_segments(x, ldx, k, seg_off, n_seg, nullptr, out.q.get(), out.k_pad,
+                               out.row_scale.get(), nonfinite_.get(), stream_);
+    else
+      launch_quantize_rows(x, ldx, k, max_rows, d_rows, out.q.get(), out.k_pad,
+                           out.row_scale.get(), nonfinite_.get(), stream_);
+  } else if (prec_ == kBF16) {
+    launch_cast_bf16(x, ldx, k, max_rows, d_rows, out.h.get(), out.k_pad, stream_);
+  } else {
+    launch_split_tf32(x, ldx, k, max_rows, d_rows, out.hi.get(), out.lo.get(), out.k_pad,
+                      stream_);
+  }
+  count();
+}
+
+void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
+                  long long ldc, const float* bias, const float* residual, int relu,
+                  long long c_step_stride, const int* d_step) {
+  auto& cache = plan_cache(this);
+  PlanKey key{a.op().ptr, w.op().ptr, m};
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, plan_gemm(a.op(), w.op(), m, w.n)).first;
+  GemmEpilogue ep{};
+  ep.C = c;
+  ep.ldc = ldc;
+  ep.c_step_stride = c_step_stride;
+  ep.d_step = d_step;
+  ep.bias = bias;
+  ep.residual = residual;
+  ep.ldr = ldc;
+  ep.a_scale = a.row_scale.get();
+  ep.w_scale = w.col_scale.get();
+  ep.relu = relu;
+  ep.M = m;
+  ep.d_M = d_m;
+  ep.N = w.n;
+  ep.vec = (ldc % 4 == 0) && (c_step_stride % 4 == 0);
+  launch_gemm(it->second, ep, stream_);
+  count();
+}
+
+// Validates and uploads sources (translate_one / beam_search / embed_source
+// preconditions: decode.cpp:38-39, model.cpp:548, tensor.cpp:456-458).
+int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status) {
+  const int n = static_cast<int>(srcs.size());
+  const ModelConfig& c = host_.config;
+  status.assign(n, 0);
+  std::vector<int> ids, pos, off(n + 1, 0), eoff(n, 0), elen(n, 0);
+  for (int s = 0; s < n; ++s) {
+    const auto& src = srcs[s];
+    if (src.empty())
+      status[s] = kUsageError;
+    else if (static_cast<int>(src.size()) > c.max_seq_len)
+      status[s] = kValueError;
+    else
+      for (int id : src)
+        if (id < 0 || id >= c.src_vocab_size) status[s] = kIndexError;
+    off[s] = static_cast<int>(ids.size());
+    eoff[s] = off[s];
+    if (status[s] == 0) {
+      for (size_t i = 0; i < src.size(); ++i) {
+        ids.push_back(src[i]);
+        pos.push_back(static_cast<int>(i));
+      }
+      elen[s] = static_cast<int>(src.size());
+    }
+  }
+  off[n] = static_cast<int>(ids.size());
+  const int m = off[n];
+  if (m) {
+    src_ids_.upload(ids.data(), m, stream_);
+    src_pos_.upload(pos.data(), m, stream_);
+  }
+  src_off_.upload(off.data(), n + 1, stream_);
+  enc_off_.upload(eoff.data(), n, stream_);
+  enc_len_.upload(elen.data(), n, stream_);
+  return m;
+}
+
+void Engine::run_encoder(int n_sent, int m, int max_src) {
+  if (m <= 0) return;
+  const ModelConfig& c = host_.config;
+  const long long d = d_;
+  const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
+  const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
+  launch_embed_src(src_ids_.get(), src_pos_.get(), m, src_embed_.get(), d_, sqrt_d, pe_.get(),
+                   enc_x_.get(), d, stream_);
+  count();
+  for (int l = 0; l < c.num_encoder_layers; ++l) {
+    EncLayer& L = enc_[l];
+    launch_layernorm(enc_x_.get(), d, m, nullptr, d_, L.n1.g.get(), L.n1.b.get(), enc_a_.get(), d,
+                     stream_);
+    count();
+    prep(enc_a_.get(), d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
+    launch_enc_attention(enc_qkv_.get(), 3 * d, src_off_.get(), n_sent, std::max(max_src, 1), d_,
+                         heads_, scale, enc_ctx_.get(), d, stream_);
+    count();
+    prep(enc_ctx_.get(), d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
+    launch_layernorm(enc_x_.get(), d, m, nullptr, d_, L.n2.g.get(), L.n2.b.get(), enc_a_.get(), d,
+                     stream_);
+    count();
+    prep(enc_a_.get(), d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
+    prep(ffh_.get(), dff_, dff_, m, nullptr, src_off_.get(), n_sent, act_ff_);
+    gemm(act_ff_, L.w2, m, nullptr, enc_x_.get(), d, L.b2.get(), enc_x_.get(), 0);
+  }
+  float* enc_out = enc_x_.get();
+  if (c.num_encoder_layers > 0) {
+    launch_layernorm(enc_x_.get(), d, m, nullptr, d_, enc_final_.g.get(), enc_final_.b.get(),
+                     enc_a_.get(), d, stream_);
+    count();
+    enc_out = enc_a_.get();
+  }
+  if (c.num_decoder_layers > 0) {
+    // init_decoder (model.cpp:598-612): one quantization of enc_out per
+    // sentence feeds every layer's cross K and V.
+    prep(enc_out, d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    for (int l = 0; l < c.num_decoder_layers; ++l)
+      gemm(act_d_, dec_[l].cross_kv, m, nullptr, ckv_[l].get(), 2 * d, nullptr, nullptr, 0);
+  }
+}
+
+void Engine::decoder_body() {
+  const ModelConfig& c = host_.config;
+  const long long d = d_;
+  const int R = r_max_;
+  const int* dr = n_rows_.get();
+  const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
+  const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
+  launch_embed_tgt(row_prev_.get(), dr, R, step_.get(), tgt_embed_f32_.get(),
+                   prec_ == kINT8 ? tgt_embed_q_.get() : nullptr, tgt_scale_, d_, sqrt_d,
+                   pe_.get(), dec_y_.get(), d, stream_);
+  count();
+  for (int l = 0; l < c.num_decoder_layers; ++l) {
+    DecLayer& L = dec_[l];
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, L.n1.g.get(), L.n1.b.get(), dec_a_.get(), d,
+                     stream_);
+    count();
+    prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    gemm(act_d_, L.self_qkv, R, dr, qkv_cache_[l].get(), 3 * d, nullptr, nullptr, 0,
+         static_cast<long long>(R) * 3 * d, step_.get());
+    launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
+                              step_.get(), d_, heads_, scale, dec_ctx_.get(), d, stream_);
+    count();
+    prep(dec_ctx_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    gemm(act_d_, L.self_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, L.n2.g.get(), L.n2.b.get(), dec_a_.get(), d,
+                     stream_);
+    count();
+    prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    gemm(act_d_, L.cross_q, R, dr, dec_cq_.get(), d, nullptr, nullptr, 0);
+    launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
+                               enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d,
+                               stream_);
+    count();
+    prep(dec_ctx_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, L.n3.g.get(), L.n3.b.get(), dec_a_.get(), d,
+                     stream_);
+    count();
+    prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
+    prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
+    gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
+  }
+  launch_layernorm(dec_y_.get(), d, R, dr, d_, dec_final_.g.get(), dec_final_.b.get(),
+                   dec_a_.get(), d, stream_);
+  count();
+  prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+  gemm(act_d_, logits_w_, R, dr, logits_.get(), Vp_, nullptr, nullptr, 0);
+}
+
+void Engine::decode_loop(int t_run) {
+  launch_beam_init(beam_, stream_);
+  count();
+  for (int t = 0; t < t_run; ++t) {
+    decoder_body();
+    launch_topk(logits_.get(), Vp_, beam_, stream_);
+    launch_beam_select(beam_, stream_);
+    launch_beam_reorder(beam_, stream_);
+    launches_ += 3;
+    if ((t + 1) % 8 == 0 && t + 1 < t_run) {
+      MTG_CUDA(cudaMemcpyAsync(h_pinned_, n_rows_.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                               stream_));
+      MTG_CUDA(cudaStreamSynchronize(stream_));
+      if (*h_pinned_ == 0) break;
+    }
+  }
+}
+
+// ============================================================================
+// public entry points
+// ============================================================================
+
+std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vector<int>>& srcs,
+                                                    const BeamConfigC& cfg) {
+  stage(srcs);
+  run_staged(cfg);
+  const int n = staged_n_;
+  std::vector<SentenceResult> out(n);
+  if (n == 0) return out;
+  std::vector<int> len(n), status(n), tok(size_t(n) * T_);
+  std::vector<float> lp(n), norm(n);
+  std::vector<unsigned> flags(n);
+  MTG_CUDA(cudaStreamSynchronize(stream_));
+  res_len_.download(len.data(), n, stream_);
+  res_status_.download(status.data(), n, stream_);
+  res_lp_.download(lp.data(), n, stream_);
+  res_norm_.download(norm.data(), n, stream_);
+  res_flags_.download(flags.data(), n, stream_);
+  res_tok_.download(tok.data(), tok.size(), stream_);
+  int bad = 0;
+  nonfinite_.download(&bad, 1, stream_);
+  for (int s = 0; s < n; ++s) {
+    SentenceResult& r = out[s];
+    if (staged_status_[s]) {
+      r.status = staged_status_[s];
+      r.flags = 4u;
+      continue;
+    }
+    r.status = bad ? kValueError : status[s];
+    r.flags = bad ? 4u : flags[s];
+    if (r.status) continue;
+    r.tokens.assign(tok.begin() + size_t(s) * T_, tok.begin() + size_t(s) * T_ + len[s]);
+    r.logprob = lp[s];
+    r.norm = norm[s];
+  }
+  return out;
+}
+
+void Engine::stage(const std::vector<std::vector<int>>& srcs) {
+  const int n = static_cast<int>(srcs.size());
+  int m = 0, max_src = 0;
+  for (const auto& s : srcs) {
+    if (static_cast<int>(s.size()) <= host_.config.max_seq_len) m += static_cast<int>(s.size());
+    max_src = std::max(max_src, static_cast<int>(s.size()));
+  }
+  ensure_workspace(n, m, std::max(cap_beam_, 1));
+  staged_ = srcs;
+  staged_n_ = n;
+  staged_m_ = stage_sources(srcs, staged_status_);
+  staged_max_src_ = std::min(max_src, host_.config.max_seq_len);
+}
+
+void Engine::run_staged(const BeamConfigC& cfg) {
+  if (cfg.beam_size < 1) fail(kUsageError, "beam_search: beam size >= 1");
+  if (cfg.beam_size > kMaxBeam)
+    fail(kUsageError, "beam size above " + std::to_string(kMaxBeam) + " is not supported");
+  const int n = staged_n_;
+  if (n == 0) return;
+  if (cfg.beam_size > cap_beam_) {
+    ensure_workspace(n, staged_m_, cfg.beam_size);
+    stage_sources(staged_, staged_status_);
+  }
+  launches_ = 0;
+  const ModelConfig& c = host_.config;
+  std::vector<int> maxlen(n, 0), done(n, 0), zero(n, 0);
+  int t_run = 0;
+  for (int s = 0; s < n; ++s) {
+    done[s] = staged_status_[s] != 0;
+    if (done[s]) continue;
+    const int sl = static_cast<int>(staged_[s].size());
+    maxlen[s] = cfg.max_len > 0 ? cfg.max_len : std::min(c.max_seq_len, sl * 2 + 5);
+    t_run = std::max(t_run, std::min(maxlen[s], c.max_seq_len));
+  }
+  sent_maxlen_.upload(maxlen.data(), n, stream_);
+  sent_done_.upload(done.data(), n, stream_);
+  res_status_.upload(zero.data(), n, stream_);
+  MTG_CUDA(cudaMemsetAsync(nonfinite_.get(), 0, sizeof(int), stream_));
+  beam_.N = n;
+  beam_.B = cfg.beam_size;
+  beam_.alpha = cfg.alpha;
+  run_encoder(n, staged_m_, staged_max_src_);
+  if (c.num_decoder_layers >= 0 && t_run > 0) decode_loop(t_run);
+  last_launches_ = launches_;
+}
+
+void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int* forced, int nf,
+                           float* out) {
+  const int n = static_cast<int>(srcs.size());
+  if (n == 0 || nf <= 0) return;
+  stage(srcs);
+  for (int s = 0; s < n; ++s)
+    if (staged_status_[s]) fail(static_cast<Status>(staged_status_[s]), "bad source sentence");
+  if (nf > host_.config.max_seq_len) fail(kValueError, "decode_step: past max_seq_len");
+  launches_ = 0;
+  MTG_CUDA(cudaMemsetAsync(nonfinite_.get(), 0, sizeof(int), stream_));
+  std::vector<int> done(n, 0);
+  sent_done_.upload(done.data(), n, stream_);
+  beam_.N = n;
+  beam_.B = 1;
+  run_encoder(n, staged_m_, staged_max_src_);
+  launch_beam_init(beam_, stream_);
+  // One hypothesis per sentence: row r = sentence r, ancestors all r.
+  std::vector<int> anc(size_t(r_max_) * T_);
+  for (int r = 0; r < r_max_; ++r)
+    for (int j = 0; j < T_; ++j) anc[size_t(r) * T_ + j] = r;
+  anc0_.upload(anc.data(), anc.size(), stream_);
+  anc1_.upload(anc.data(), anc.size(), stream_);
+  std::vector<float> rows(size_t(n) * Vp_);
+  std::vector<int> prev(n);
+  for (int t = 0; t < nf; ++t) {
+    decoder_body();
+    MTG_CUDA(cudaStreamSynchronize(stream_));
+    logits_.download(rows.data(), rows.size(), stream_);
+    for (int s = 0; s < n; ++s)
+      std::copy(rows.begin() + size_t(s) * Vp_, rows.begin() + size_t(s) * Vp_ + V_,
+                out + (size_t(s) * nf + t) * V_);
+    for (int s = 0; s < n; ++s) prev[s] = forced[t];
+    row_prev_.upload(prev.data(), n, stream_);
+    const int next = t + 1;
+    step_.upload(&next, 1, stream_);
+  }
+  int bad = 0;
+  nonfinite_.download(&bad, 1, stream_);
+  if (bad) fail(kValueError, "quantize: non-finite values in tensor");
+  last_launches_ = launches_;
+}
+
+void Engine::encode(const std::vector<std::vector<int>>& srcs, float* out) {
+  const int n = static_cast<int>(srcs.size());
+  if (n == 0) return;
+  stage(srcs);
+  for (int s = 0; s < n; ++s)
+    if (staged_status_[s]) fail(static_cast<Status>(staged_status_[s]), "bad source sentence");
+  MTG_CUDA(cudaMemsetAsync(nonfinite_.get(), 0, sizeof(int), stream_));
+  run_encoder(n, staged_m_, staged_max_src_);
+  MTG_CUDA(cudaStreamSynchronize(stream_));
+  const float* src = host_.config.num_encoder_layers > 0 ? enc_a_.get() : enc_x_.get();
+  MTG_CUDA(cudaMemcpy(out, src, sizeof(float) * size_t(staged_m_) * d_, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace mtg

@@ -1,0 +1,156 @@
+// The device engine: weights laid out K-major for the tcgen05 GEMM, a
+// workspace sized per batch, the batched encoder, and the device-resident
+// beam-search step loop. One engine = one model on one device + one stream.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "device_buffer.hpp"
+#include "gemm.hpp"
+#include "kernels.cuh"
+#include "model_host.hpp"
+
+namespace mtg {
+
+enum Precision : int { kF32 = 0, kBF16 = 1, kINT8 = 2 };  // == MTG_PREC_*
+
+// One GEMM weight [N x K] (K-major), possibly the concatenation of several
+// reference tensors along N (q|k|v, k|v).
+struct DevLinear {
+  int n = 0, k = 0, k_pad = 0, prec = 0;
+  DeviceBuffer<int8_t> q;
+  DeviceBuffer<__nv_bfloat16> h;
+  DeviceBuffer<float> hi, lo;
+  DeviceBuffer<float> col_scale;  // int8: per-column weight scale
+  Operand op() const;
+};
+
+// GEMM activation operand buffer for a given K.
+struct ActOperand {
+  int rows = 0, k = 0, k_pad = 0, prec = 0;
+  DeviceBuffer<int8_t> q;
+  DeviceBuffer<__nv_bfloat16> h;
+  DeviceBuffer<float> hi, lo;
+  DeviceBuffer<float> row_scale;
+  Operand op() const;
+  void allocate(int rows, int k, int prec);
+};
+
+struct BeamConfigC {
+  int beam_size = 4;
+  int max_len = 0;  // <= 0: derive per sentence
+  float alpha = 1.0f;
+};
+
+struct SentenceResult {
+  std::vector<int> tokens;
+  float logprob = 0.0f;
+  float norm = 0.0f;
+  unsigned flags = 0;
+  int status = 0;
+};
+
+class Engine {
+ public:
+  Engine(HostModel model, int precision, int device);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const ModelConfig& config() const { return host_.config; }
+  int precision() const { return prec_; }
+  const HostModel& host_model() const { return host_; }
+  std::mutex& mutex() { return mu_; }
+
+  // Batched beam search over one device batch (sources carry their EOS).
+  std::vector<SentenceResult> translate_batch(const std::vector<std::vector<int>>& srcs,
+                                              const BeamConfigC& cfg);
+  // decode_step logits along forced prefixes; out[(i*nf + t)*V + v].
+  void forced_logits(const std::vector<std::vector<int>>& srcs, const int* forced, int nf,
+                     float* out);
+  // encode_infer(embed_source_infer(.)) rows.
+  void encode(const std::vector<std::vector<int>>& srcs, float* out);
+
+  // Benchmark support: keep a staged batch resident and re-run it.
+  void stage(const std::vector<std::vector<int>>& srcs);
+  void run_staged(const BeamConfigC& cfg);
+  int64_t last_launches() const { return last_launches_; }
+  cudaStream_t stream() const { return stream_; }
+
+ private:
+  struct Layer;  // device weights of one layer
+  void upload_weights();
+  void ensure_workspace(int n_sent, int m_enc, int beam);
+  void prep(const float* x, long long ldx, int k, int max_rows, const int* d_rows,
+            const int* seg_off, int n_seg, ActOperand& out);
+  void gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
+            long long ldc, const float* bias, const float* residual, int relu,
+            long long c_step_stride = 0, const int* d_step = nullptr);
+  int stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status);
+  void run_encoder(int n_sent, int m_enc, int max_src);
+  void decoder_body();  // decoder layers + dec_final + logits for the live rows
+  void decode_loop(int t_run);
+  void count() { ++launches_; }
+
+  HostModel host_;
+  int prec_;
+  int device_;
+  cudaStream_t stream_ = nullptr;
+  std::mutex mu_;
+  int64_t launches_ = 0, last_launches_ = 0;
+
+  // ---- weights ----
+  DeviceBuffer<float> src_embed_, tgt_embed_f32_, pe_;
+  DeviceBuffer<int8_t> tgt_embed_q_;
+  float tgt_scale_ = 1.0f;
+  DevLinear logits_w_;
+  struct LN {
+    DeviceBuffer<float> g, b;
+  };
+  struct EncLayer {
+    LN n1, n2;
+    DevLinear qkv, wo, w1, w2;
+    DeviceBuffer<float> b1, b2;
+  };
+  struct DecLayer {
+    LN n1, n2, n3;
+    DevLinear self_qkv, self_wo, cross_q, cross_kv, cross_wo, w1, w2;
+    DeviceBuffer<float> b1, b2;
+  };
+  std::vector<EncLayer> enc_;
+  std::vector<DecLayer> dec_;
+  LN enc_final_, dec_final_;
+
+  // ---- workspace ----
+  int cap_sent_ = 0, cap_enc_ = 0, cap_beam_ = 0, r_max_ = 0, act_rows_ = 0;
+  int d_ = 0, dff_ = 0, V_ = 0, Vp_ = 0, T_ = 0, heads_ = 0;
+  ActOperand act_d_, act_ff_;
+  DeviceBuffer<float> enc_x_, enc_a_, enc_qkv_, enc_ctx_, ffh_;
+  std::vector<DeviceBuffer<float>> ckv_;
+  DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;
+  std::vector<DeviceBuffer<float>> qkv_cache_;
+  DeviceBuffer<int> src_ids_, src_pos_, src_off_, enc_off_, enc_len_;
+  DeviceBuffer<int> nonfinite_;
+  // beam state
+  DeviceBuffer<int> step_, n_rows_, row_sent_, row_prev_, row_parent_, anc0_, anc1_, tok0_, tok1_,
+      cand_tok_, sent_row0_, sent_live_, sent_maxlen_, sent_done_, best_has_, best_len_, best_tok_,
+      res_len_, res_status_, res_tok_, sel_parent_, sel_tok_;
+  DeviceBuffer<float> row_lp_, cand_score_, best_norm_, best_lp_, res_lp_, res_norm_, sel_lp_;
+  DeviceBuffer<unsigned> res_flags_;
+  BeamDev beam_{};
+  int* h_pinned_ = nullptr;  // pinned host mailbox (n_rows polling)
+
+  // staged batch (benchmark)
+  std::vector<std::vector<int>> staged_;
+  int staged_m_ = 0, staged_max_src_ = 0, staged_n_ = 0;
+  std::vector<int> staged_status_;
+};
+
+}  // namespace mtg

@@ -42,6 +42,7 @@ struct GemmEpilogue {
   int M;                     // rows, unless d_M != null
   const int* d_M;
   int N;
+  int vec;                   // 1: C/residual rows are 16-byte aligned (float4 path)
 };
 
 enum GemmPrec : int { kPrecI8 = 0, kPrecBF16 = 1, kPrecTF32x3 = 2 };
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           v[j] = __uint_as_float(r[j]);
         }
       }
-      const bool full = (col0 + 16 <= ep.N);
+      const bool full = ep.vec && (col0 + 16 <= ep.N);
       if (ep.bias) {
 #pragma unroll
         for (int j = 0; j < 16; ++j)

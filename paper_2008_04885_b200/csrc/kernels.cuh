@@ -1,0 +1,103 @@
+// Non-GEMM kernels of the translation hot path. Float reduction orders are
+// pinned so the CPU oracle reproduces them bit for bit.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mtg {
+
+constexpr int kMaxBeam = 16;
+
+// ---- embeddings (model.cpp:539-581, 624-626) -----------------------------------
+
+// out[r] = table[ids[r]] * sqrt_d + pe[pos[r]]
+void launch_embed_src(const int* ids, const int* pos, int rows, const float* table, int d,
+                      float sqrt_d, const float* pe, float* out, long long ldo,
+                      cudaStream_t st);
+
+// Decoder input rows (d_rows on device), position = *d_step. table_q != null:
+// int8 table dequantised as q / scale (model.cpp:485).
+void launch_embed_tgt(const int* prev, const int* d_rows, int max_rows, const int* d_step,
+                      const float* table, const int8_t* table_q, float q_scale, int d,
+                      float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st);
+
+// ---- layer norm (tensor.cpp:368-387) -------------------------------------------
+void launch_layernorm(const float* x, long long ldx, int max_rows, const int* d_rows, int n,
+                      const float* g, const float* b, float* y, long long ldy, cudaStream_t st);
+
+// ---- attention (model.cpp:509-528, 642-665) ------------------------------------
+
+// Encoder self-attention over each sentence (rows off[s]..off[s+1]).
+// qkv rows: [q | k | v] each d wide, pitch ldq. ctx pitch ldc.
+void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
+                          int max_len, int d, int heads, float scale, float* ctx,
+                          long long ldc, cudaStream_t st);
+
+// Decoder self-attention for live row r at step t over positions 0..t; the key
+// of position j lives in row anc[r*T + j] of the step-j slab of qkv_cache
+// ([T][R_max][3d]). anc0/anc1: the double-buffered ancestor tables (t & 1).
+void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const int* anc0,
+                               const int* anc1, const int* d_rows, const int* d_step, int d,
+                               int heads, float scale, float* ctx, long long ldc,
+                               cudaStream_t st);
+
+// Decoder cross-attention: row r attends to its sentence's encoder rows
+// (enc_off[s]..+enc_len[s]) in ckv ([M_enc][2d] = [k | v]).
+void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv,
+                                const int* row_sent, const int* enc_off, const int* enc_len,
+                                const int* d_rows, int max_rows, int max_src, int d, int heads,
+                                float scale, float* ctx, long long ldc, cudaStream_t st);
+
+// ---- beam search (decode.cpp:25-109) -------------------------------------------
+
+struct BeamDev {
+  int* step;        // [1]
+  int* n_rows;      // [1]
+  int* row_sent;    // [R_max]
+  float* row_lp;    // [R_max]
+  int* row_prev;    // [R_max]
+  int* row_parent;  // [R_max]
+  int* anc[2];      // [R_max * T]
+  int* tok[2];      // [R_max * T]
+  float* cand_score;  // [R_max * B]
+  int* cand_tok;      // [R_max * B]
+  int* sent_row0;     // [N]
+  int* sent_live;     // [N]
+  int* sent_maxlen;   // [N]
+  int* sent_done;     // [N]
+  int* best_has;      // [N]
+  float* best_norm;
+  float* best_lp;
+  int* best_len;
+  int* best_tok;      // [N * T]
+  int* res_len;       // [N]
+  float* res_lp;
+  float* res_norm;
+  unsigned* res_flags;
+  int* res_status;
+  int* res_tok;       // [N * T]
+  int* sel_parent;    // [N * B]
+  int* sel_tok;
+  float* sel_lp;
+  int N, B, T, R_max, V;
+  float alpha;
+  int max_seq_len;
+};
+
+// Step 0: one root row (BOS, logprob 0) per active sentence.
+void launch_beam_init(const BeamDev& b, cudaStream_t st);
+
+// log_softmax_row + candidate scores + per-row top-min(B,V) by (score desc,
+// token asc); one 1024-thread CTA per live row.
+void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st);
+
+// Per-sentence selection of beam_size candidates by (score desc, parent asc,
+// token asc), EOS -> finished (running first-max of the GNMT score), live
+// rows compacted in rank order, termination + result extraction; step += 1.
+void launch_beam_select(const BeamDev& b, cudaStream_t st);
+
+// Gathers ancestor-row and token histories of the new rows from their parents.
+void launch_beam_reorder(const BeamDev& b, cudaStream_t st);
+
+}  // namespace mtg
