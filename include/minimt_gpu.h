@@ -144,6 +144,15 @@ int mtg_stage_sources(mtg_model* m, const int32_t* src_ids, const int64_t* src_o
 int mtg_translate_staged(mtg_model* m, const mtg_beam_config* cfg);
 /* Kernel launches issued by the last translate call (for gpu_launches). */
 int64_t mtg_last_launch_count(const mtg_model* m);
+/* The handle's CUDA stream (cudaStream_t as void*), for event timing. */
+void* mtg_model_stream(const mtg_model* m);
+/* Times `iters` back-to-back launches of one hot kernel on the staged batch
+ * (kernel: 0 = decoder output-projection GEMM, 1 = log-softmax/top-k,
+ * 2 = decoder self-attention, 3 = encoder FFN w1 GEMM) with CUDA events on
+ * the handle's stream. Writes the mean milliseconds per launch and the
+ * algorithmic bytes and FLOPs of one launch. */
+int mtg_time_kernel(mtg_model* m, int kernel, int iters, float* ms_per_launch,
+                    double* bytes_per_launch, double* flops_per_launch);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@ using namespace orc;
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_code = 0;
 
 struct Handle {
   std::unique_ptr<Model> f32;
@@ -44,9 +45,11 @@ int guard(F&& f) {
     return 0;
   } catch (const Error& e) {
     g_err = e.what();
+    g_code = e.code;
     return e.code;
   } catch (const std::exception& e) {
     g_err = e.what();
+    g_code = kState;
     return kState;
   }
 }
@@ -69,6 +72,7 @@ void write_hyp(const Hypothesis& h, float alpha, int* out_tokens, int cap, int* 
 extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
+int orc_last_error_code(void) { return g_code; }
 
 void* orc_model_create(const char* cfg_json, uint64_t seed, int do_init) {
   Handle* h = nullptr;

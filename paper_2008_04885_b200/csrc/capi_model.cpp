@@ -158,4 +158,17 @@ int64_t mtg_last_launch_count(const mtg_model* m) {
   return m && m->eng ? m->eng->last_launches() : -1;
 }
 
+void* mtg_model_stream(const mtg_model* m) {
+  return m && m->eng ? static_cast<void*>(m->eng->stream()) : nullptr;
+}
+
+int mtg_time_kernel(mtg_model* m, int kernel, int iters, float* ms_per_launch,
+                    double* bytes_per_launch, double* flops_per_launch) {
+  return guarded([&] {
+    Engine& e = engine(m);
+    std::lock_guard<std::mutex> lock(e.mutex());
+    e.time_kernel(kernel, iters, ms_per_launch, bytes_per_launch, flops_per_launch);
+  });
+}
+
 }  // extern "C"

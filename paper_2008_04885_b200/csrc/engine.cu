@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <map>
 #include <tuple>
 
@@ -627,8 +628,73 @@ void Engine::run_staged(const BeamConfigC& cfg) {
   beam_.B = cfg.beam_size;
   beam_.alpha = cfg.alpha;
   run_encoder(n, staged_m_, staged_max_src_);
-  if (c.num_decoder_layers >= 0 && t_run > 0) decode_loop(t_run);
+  if (t_run > 0) decode_loop(t_run);
   last_launches_ = launches_;
+  last_beam_ = cfg.beam_size;
+  last_t_run_ = t_run;
+}
+
+void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double* flops) {
+  if (staged_n_ == 0 || last_beam_ == 0)
+    fail(kStateError, "time_kernel: stage a batch and run it once first");
+  if (iters < 1) fail(kUsageError, "time_kernel: iters >= 1");
+  const ModelConfig& c = host_.config;
+  const int R = staged_n_ * last_beam_;
+  const int eb = prec_elem_bytes(gemm_prec_of(prec_));
+  const int split = prec_ == kF32 ? 2 : 1;  // hi + lo operands
+  scratch_rows_.resize(1);
+  scratch_rows_.upload(&R, 1, stream_);
+  cudaEvent_t e0, e1;
+  MTG_CUDA(cudaEventCreate(&e0));
+  MTG_CUDA(cudaEventCreate(&e1));
+  std::function<void()> launch;
+  if (kernel == 0) {  // decoder output projection (tied tgt_embed)
+    launch = [&] {
+      gemm(act_d_, logits_w_, r_max_, scratch_rows_.get(), logits_.get(), Vp_, nullptr, nullptr, 0);
+    };
+    *bytes = double(split) * eb * (double(V_) * logits_w_.k_pad + double(R) * act_d_.k_pad) +
+             4.0 * R * V_;
+    *flops = 2.0 * R * V_ * d_ * (prec_ == kF32 ? 3 : 1);
+  } else if (kernel == 1) {  // log-softmax + top-k over R x V logits
+    n_rows_.upload(&R, 1, stream_);
+    launch = [&] { launch_topk(logits_.get(), Vp_, beam_, stream_); };
+    *bytes = 4.0 * R * V_;
+    *flops = 0.0;
+  } else if (kernel == 2) {  // decoder self-attention at the last step
+    if (c.num_decoder_layers == 0) fail(kStateError, "no decoder layers");
+    const int t = std::max(0, last_t_run_ - 1);
+    n_rows_.upload(&R, 1, stream_);
+    step_.upload(&t, 1, stream_);
+    const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
+    launch = [&, scale] {
+      launch_dec_self_attention(qkv_cache_[0].get(), r_max_, T_, anc0_.get(), anc1_.get(),
+                                n_rows_.get(), step_.get(), d_, heads_, scale, dec_ctx_.get(), d_,
+                                stream_);
+    };
+    *bytes = 4.0 * R * (double(t + 1) * 2 * d_ + 2.0 * d_);
+    *flops = 4.0 * R * (t + 1) * d_;
+  } else if (kernel == 3) {  // encoder FFN w1 GEMM
+    if (c.num_encoder_layers == 0) fail(kStateError, "no encoder layers");
+    const int M = staged_m_;
+    launch = [&, M] {
+      gemm(act_d_, enc_[0].w1, M, nullptr, ffh_.get(), dff_, enc_[0].b1.get(), nullptr, 1);
+    };
+    *bytes = double(split) * eb * (double(dff_) * enc_[0].w1.k_pad + double(M) * act_d_.k_pad) +
+             4.0 * M * dff_;
+    *flops = 2.0 * M * dff_ * d_ * (prec_ == kF32 ? 3 : 1);
+  } else {
+    fail(kUsageError, "time_kernel: unknown kernel id");
+  }
+  launch();  // warm
+  MTG_CUDA(cudaEventRecord(e0, stream_));
+  for (int i = 0; i < iters; ++i) launch();
+  MTG_CUDA(cudaEventRecord(e1, stream_));
+  MTG_CUDA(cudaEventSynchronize(e1));
+  float total = 0.0f;
+  MTG_CUDA(cudaEventElapsedTime(&total, e0, e1));
+  *ms = total / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
 }
 
 void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int* forced, int nf,

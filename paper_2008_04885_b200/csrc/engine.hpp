@@ -83,6 +83,8 @@ class Engine {
   void run_staged(const BeamConfigC& cfg);
   int64_t last_launches() const { return last_launches_; }
   cudaStream_t stream() const { return stream_; }
+  // Times one hot kernel in isolation on the staged batch (see minimt_gpu.h).
+  void time_kernel(int kernel, int iters, float* ms, double* bytes, double* flops);
 
  private:
   struct Layer;  // device weights of one layer
@@ -151,6 +153,8 @@ class Engine {
   std::vector<std::vector<int>> staged_;
   int staged_m_ = 0, staged_max_src_ = 0, staged_n_ = 0;
   std::vector<int> staged_status_;
+  int last_beam_ = 0, last_t_run_ = 0;
+  DeviceBuffer<int> scratch_rows_;  // fixed row count for kernel timing
 };
 
 }  // namespace mtg

@@ -92,7 +92,7 @@ def i32(x) -> np.ndarray:
 class OracleModel:
     def __init__(self, handle):
         if not handle:
-            raise OracleError(4, (lib.orc_last_error() or b"").decode())
+            raise OracleError(lib.orc_last_error_code(), (lib.orc_last_error() or b"").decode())
         self.h = ctypes.c_void_p(handle)
         buf = ctypes.create_string_buffer(4096)
         check(lib.orc_model_config_json(self.h, buf, 4096))
