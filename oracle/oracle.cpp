@@ -4,9 +4,10 @@
 // this file agree on the ones below):
 //   P1 lane sum     : 32 partials, partial l = sum of v[l], v[l+32], ... in
 //                     order, then xor-butterfly (16,8,4,2,1). (warp_sum)
-//   P2 block sum    : 1024 partials, partial t = sum over i of v[4(t+1024i)+c],
+//   P2 block sum    : 512 partials, partial t = sum over i of v[4(t+512i)+c],
 //                     c = 0..3, in order; P1 butterfly per 32-thread warp, then
-//                     P1 butterfly across the 32 warp sums. (block_sum_1024)
+//                     P1 butterfly across the 16 warp sums (+16 zero lanes).
+//                     (block_sum_512)
 //   P3 dot          : acc = 0; acc = acc + a[c]*b[c] for c ascending (no FMA).
 //   P4 exp/log/pow  : detmath.h.
 //   P5 f32 GEMM     : per output element, k-ascending mul+add (gemm_rows order,
@@ -684,18 +685,20 @@ float butterfly32(float* p) {
   return p[0];
 }
 
-// P2
-float block_sum_1024(const float* v, Index n) {
-  static thread_local std::vector<float> part(1024);
-  for (int t = 0; t < 1024; ++t) {
+// P2 (512 threads = 16 warps; the 16 warp sums are butterflied in one warp
+// with lanes 16..31 contributing 0).
+float block_sum_512(const float* v, Index n) {
+  constexpr int kT = 512;
+  static thread_local std::vector<float> part(kT);
+  for (int t = 0; t < kT; ++t) {
     float s = 0.0f;
-    for (Index base = 4LL * t; base < n; base += 4LL * 1024)
+    for (Index base = 4LL * t; base < n; base += 4LL * kT)
       for (int c = 0; c < 4; ++c)
         if (base + c < n) s = s + v[base + c];
     part[t] = s;
   }
   float ws[32];
-  for (int w = 0; w < 32; ++w) ws[w] = butterfly32(&part[w * 32]);
+  for (int w = 0; w < 32; ++w) ws[w] = w < kT / 32 ? butterfly32(&part[w * 32]) : 0.0f;
   return butterfly32(ws);
 }
 
@@ -1100,7 +1103,7 @@ std::vector<float> log_softmax_row(const float* x, int n) {
   for (int j = 0; j < n; ++j) mx = std::max(mx, x[j]);
   std::vector<float> e(static_cast<size_t>(n));
   for (int j = 0; j < n; ++j) e[j] = orc_expf(x[j] - mx);
-  const float lse = orc_logf(block_sum_1024(e.data(), n)) + mx;
+  const float lse = orc_logf(block_sum_512(e.data(), n)) + mx;
   for (int j = 0; j < n; ++j) e[j] = x[j] - lse;
   return e;
 }

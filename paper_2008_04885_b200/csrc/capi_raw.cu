@@ -62,10 +62,10 @@ void run_i8(const std::vector<int8_t>& a_kmaj, float sa, const std::vector<int8_
   ep.C = dc.get();
   ep.ldc = ldc;
   ep.a_scale = dsa.get();
-  ep.w_scale = dsb.get();
+  ep.w_seg_scale = dsb.get();  // one weight tensor: a single segment
+  ep.seg_width = 0;
   ep.M = m;
   ep.N = n;
-  ep.vec = 1;
   launch_gemm(plan, ep, 0);
   MTG_CUDA(cudaDeviceSynchronize());
   std::vector<float> hc(static_cast<size_t>(std::max(m, 1)) * ldc);
@@ -185,7 +185,6 @@ int mtg_gemm(int precision, const float* a, const float* b, int m, int k, int n,
     ep.ldc = ldc;
     ep.M = m;
     ep.N = n;
-    ep.vec = 1;
     launch_gemm(plan, ep, 0);
     MTG_CUDA(cudaDeviceSynchronize());
     std::vector<float> hc(size_t(m) * ldc);

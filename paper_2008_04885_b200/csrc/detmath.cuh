@@ -36,6 +36,30 @@ __device__ __forceinline__ float det_expf(float x) {
   return p;
 }
 
+// det_expf for finite x <= 0 (softmax arguments x - max): same bits, minus
+// the NaN / overflow branches.
+__device__ __forceinline__ float det_expf_nonpos(float x) {
+  if (x < -103.97208404541015625f) return 0.0f;
+  const float n = rintf(__fmul_rn(x, 1.44269502162933349609375f));
+  float r = __fmaf_rn(n, -0.693359375f, x);
+  r = __fmaf_rn(n, 2.12194440e-4f, r);
+  const float z = __fmul_rn(r, r);
+  float p = 1.9875691500e-4f;
+  p = __fmaf_rn(p, r, 1.3981999507e-3f);
+  p = __fmaf_rn(p, r, 8.3334519073e-3f);
+  p = __fmaf_rn(p, r, 4.1665795894e-2f);
+  p = __fmaf_rn(p, r, 1.6666665459e-1f);
+  p = __fmaf_rn(p, r, 5.0000001201e-1f);
+  p = __fmaf_rn(p, z, r);
+  p = __fadd_rn(p, 1.0f);
+  const int ni = static_cast<int>(n);
+  const int n1 = ni / 2;
+  const int n2 = ni - n1;
+  p = __fmul_rn(p, __int_as_float((n1 + 127) << 23));
+  p = __fmul_rn(p, __int_as_float((n2 + 127) << 23));
+  return p;
+}
+
 __device__ __forceinline__ float det_logf(float x) {
   if (x != x) return x;
   if (x < 0.0f) return __int_as_float(0x7fc00000);

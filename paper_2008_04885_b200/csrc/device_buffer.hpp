@@ -39,7 +39,11 @@ class DeviceBuffer {
     release();
     if (n) {
       MTG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+      // cudaMemset runs on the legacy default stream, which is not ordered
+      // with the engine's non-blocking stream: finish it before returning so
+      // it cannot land after later writes.
       MTG_CUDA(cudaMemset(p_, 0, n * sizeof(T)));
+      MTG_CUDA(cudaDeviceSynchronize());
     }
     n_ = n;
   }

@@ -50,13 +50,24 @@ void build_linear(DevLinear& L, const std::vector<const HostTensor*>& parts, boo
   L.k_pad = pad_k(k, L.prec);
   if (prec == kINT8) {
     std::vector<int8_t> buf(size_t(n) * L.k_pad, 0);
-    std::vector<float> cs(n);
+    // One max-abs scale per reference tensor; fused tensors are equal-width
+    // column segments (q|k|v, k|v).
+    std::vector<float> seg(kMaxSegments, 1.0f);
+    if (parts.size() > static_cast<size_t>(kMaxSegments))
+      fail(kStateError, "too many fused weight segments");
+    L.seg_width = parts.size() > 1 ? static_cast<int>(nt ? parts[0]->rows() : parts[0]->cols()) : 0;
+    for (size_t i = 0; i < parts.size(); ++i) {
+      seg[i] = parts[i]->scale;
+      const int pn = static_cast<int>(nt ? parts[i]->rows() : parts[i]->cols());
+      if (parts.size() > 1 && pn != L.seg_width) fail(kStateError, "unequal fused segments");
+    }
+    L.seg_scale.resize(kMaxSegments);
+    L.seg_scale.upload(seg.data(), kMaxSegments);
     int n0 = 0;
     for (auto* p : parts) {
       if (!p->is_int8) fail(kStateError, "no quantized copy of a weight");
       const int pn = static_cast<int>(nt ? p->rows() : p->cols());
       for (int j = 0; j < pn; ++j) {
-        cs[n0 + j] = p->scale;
         int8_t* dst = buf.data() + size_t(n0 + j) * L.k_pad;
         if (nt)
           std::copy(p->q.begin() + size_t(j) * k, p->q.begin() + size_t(j + 1) * k, dst);
@@ -67,8 +78,6 @@ void build_linear(DevLinear& L, const std::vector<const HostTensor*>& parts, boo
     }
     L.q.resize(buf.size());
     L.q.upload(buf.data(), buf.size());
-    L.col_scale.resize(n);
-    L.col_scale.upload(cs.data(), n);
   } else {
     std::vector<float> kmaj(size_t(n) * k);
     int n0 = 0;
@@ -269,6 +278,8 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   qkv_cache_.resize(c.num_decoder_layers);
   for (auto& b : qkv_cache_) b.resize(size_t(T_) * r_max_ * 3 * d);
   src_ids_.resize(M);
+  src_rowseg_.resize(M);
+  rowmax_.resize(act_rows_);
   src_pos_.resize(M);
   src_off_.resize(N + 1);
   enc_off_.resize(N);
@@ -384,12 +395,12 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   ep.residual = residual;
   ep.ldr = ldc;
   ep.a_scale = a.row_scale.get();
-  ep.w_scale = w.col_scale.get();
+  ep.w_seg_scale = w.seg_scale.get();
+  ep.seg_width = w.seg_width;
   ep.relu = relu;
   ep.M = m;
   ep.d_M = d_m;
   ep.N = w.n;
-  ep.vec = (ldc % 4 == 0) && (c_step_stride % 4 == 0);
   launch_gemm(it->second, ep, stream_);
   count();
 }
@@ -400,7 +411,7 @@ int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector
   const int n = static_cast<int>(srcs.size());
   const ModelConfig& c = host_.config;
   status.assign(n, 0);
-  std::vector<int> ids, pos, off(n + 1, 0), eoff(n, 0), elen(n, 0);
+  std::vector<int> ids, pos, seg, off(n + 1, 0), eoff(n, 0), elen(n, 0);
   for (int s = 0; s < n; ++s) {
     const auto& src = srcs[s];
     if (src.empty())
@@ -416,6 +427,7 @@ int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector
       for (size_t i = 0; i < src.size(); ++i) {
         ids.push_back(src[i]);
         pos.push_back(static_cast<int>(i));
+        seg.push_back(s);
       }
       elen[s] = static_cast<int>(src.size());
     }
@@ -425,11 +437,56 @@ int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector
   if (m) {
     src_ids_.upload(ids.data(), m, stream_);
     src_pos_.upload(pos.data(), m, stream_);
+    src_rowseg_.upload(seg.data(), m, stream_);
   }
   src_off_.upload(off.data(), n + 1, stream_);
   enc_off_.upload(eoff.data(), n, stream_);
   enc_len_.upload(elen.data(), n, stream_);
   return m;
+}
+
+OperandOut Engine::opout(ActOperand& a) {
+  OperandOut o;
+  o.prec = a.prec;
+  o.k_pad = a.k_pad;
+  o.q = a.q.get();
+  o.row_scale = a.row_scale.get();
+  o.h = a.h.get();
+  o.hi = a.hi.get();
+  o.lo = a.lo.get();
+  o.nonfinite = nonfinite_.get();
+  return o;
+}
+
+// Encoder operand for the next GEMM. int8: one scale per sentence (the
+// reference quantizes the [S x k] tensor its Executor::linear receives).
+void Engine::prep_enc(const float* x, long long ldx, int k, int m, ActOperand& out,
+                      bool have_rowmax) {
+  if (prec_ == kINT8) {
+    if (!have_rowmax) {
+      launch_rowmax(x, ldx, m, k, rowmax_.get(), nonfinite_.get(), stream_);
+      count();
+    }
+    launch_quantize_seg(x, ldx, m, k, src_rowseg_.get(), src_off_.get(), rowmax_.get(),
+                        opout(out), stream_);
+    count();
+  } else {
+    prep(x, ldx, k, m, nullptr, nullptr, 0, out);
+  }
+}
+
+// Encoder LayerNorm; int8 also records per-row max |y| for the segment scale.
+void Engine::ln_enc(const float* x, int m, const LN& ln, float* y, ActOperand& out) {
+  if (prec_ == kINT8) {
+    launch_layernorm(x, d_, m, nullptr, d_, ln.g.get(), ln.b.get(), y, d_, rowmax_.get(),
+                     nullptr, stream_);
+    count();
+    prep_enc(y, d_, d_, m, out, true);
+  } else {
+    const OperandOut o = opout(out);
+    launch_layernorm(x, d_, m, nullptr, d_, ln.g.get(), ln.b.get(), y, d_, nullptr, &o, stream_);
+    count();
+  }
 }
 
 void Engine::run_encoder(int n_sent, int m, int max_src) {
@@ -443,38 +500,34 @@ void Engine::run_encoder(int n_sent, int m, int max_src) {
   count();
   for (int l = 0; l < c.num_encoder_layers; ++l) {
     EncLayer& L = enc_[l];
-    launch_layernorm(enc_x_.get(), d, m, nullptr, d_, L.n1.g.get(), L.n1.b.get(), enc_a_.get(), d,
-                     stream_);
-    count();
-    prep(enc_a_.get(), d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    ln_enc(enc_x_.get(), m, L.n1, enc_a_.get(), act_d_);
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
     launch_enc_attention(enc_qkv_.get(), 3 * d, src_off_.get(), n_sent, std::max(max_src, 1), d_,
                          heads_, scale, enc_ctx_.get(), d, stream_);
     count();
-    prep(enc_ctx_.get(), d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    prep_enc(enc_ctx_.get(), d, d_, m, act_d_, false);
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
-    launch_layernorm(enc_x_.get(), d, m, nullptr, d_, L.n2.g.get(), L.n2.b.get(), enc_a_.get(), d,
-                     stream_);
-    count();
-    prep(enc_a_.get(), d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
+    ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
     gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
-    prep(ffh_.get(), dff_, dff_, m, nullptr, src_off_.get(), n_sent, act_ff_);
+    prep_enc(ffh_.get(), dff_, dff_, m, act_ff_, false);
     gemm(act_ff_, L.w2, m, nullptr, enc_x_.get(), d, L.b2.get(), enc_x_.get(), 0);
   }
-  float* enc_out = enc_x_.get();
-  if (c.num_encoder_layers > 0) {
-    launch_layernorm(enc_x_.get(), d, m, nullptr, d_, enc_final_.g.get(), enc_final_.b.get(),
-                     enc_a_.get(), d, stream_);
-    count();
-    enc_out = enc_a_.get();
+  if (c.num_decoder_layers == 0) {
+    if (c.num_encoder_layers > 0) {
+      launch_layernorm(enc_x_.get(), d, m, nullptr, d_, enc_final_.g.get(), enc_final_.b.get(),
+                       enc_a_.get(), d, nullptr, nullptr, stream_);
+      count();
+    }
+    return;
   }
-  if (c.num_decoder_layers > 0) {
-    // init_decoder (model.cpp:598-612): one quantization of enc_out per
-    // sentence feeds every layer's cross K and V.
-    prep(enc_out, d, d_, m, nullptr, src_off_.get(), n_sent, act_d_);
-    for (int l = 0; l < c.num_decoder_layers; ++l)
-      gemm(act_d_, dec_[l].cross_kv, m, nullptr, ckv_[l].get(), 2 * d, nullptr, nullptr, 0);
-  }
+  // init_decoder (model.cpp:598-612): one quantization of enc_out per
+  // sentence feeds every layer's cross K and V.
+  if (c.num_encoder_layers > 0)
+    ln_enc(enc_x_.get(), m, enc_final_, enc_a_.get(), act_d_);
+  else
+    prep_enc(enc_x_.get(), d, d_, m, act_d_, false);
+  for (int l = 0; l < c.num_decoder_layers; ++l)
+    gemm(act_d_, dec_[l].cross_kv, m, nullptr, ckv_[l].get(), 2 * d, nullptr, nullptr, 0);
 }
 
 void Engine::decoder_body() {
@@ -488,42 +541,37 @@ void Engine::decoder_body() {
                    prec_ == kINT8 ? tgt_embed_q_.get() : nullptr, tgt_scale_, d_, sqrt_d,
                    pe_.get(), dec_y_.get(), d, stream_);
   count();
+  // Decoder rows are their own quantization segments (one hypothesis row per
+  // Executor::linear call in decode_step), so LayerNorm and attention write
+  // the next GEMM's operand directly.
+  const OperandOut od = opout(act_d_);
+  auto ln_dec = [&](const LN& ln) {
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), dec_a_.get(), d, nullptr,
+                     &od, stream_);
+    count();
+  };
   for (int l = 0; l < c.num_decoder_layers; ++l) {
     DecLayer& L = dec_[l];
-    launch_layernorm(dec_y_.get(), d, R, dr, d_, L.n1.g.get(), L.n1.b.get(), dec_a_.get(), d,
-                     stream_);
-    count();
-    prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    ln_dec(L.n1);
     gemm(act_d_, L.self_qkv, R, dr, qkv_cache_[l].get(), 3 * d, nullptr, nullptr, 0,
          static_cast<long long>(R) * 3 * d, step_.get());
     launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
-                              step_.get(), d_, heads_, scale, dec_ctx_.get(), d, stream_);
+                              step_.get(), d_, heads_, scale, dec_ctx_.get(), d, od, stream_);
     count();
-    prep(dec_ctx_.get(), d, d_, R, dr, nullptr, 0, act_d_);
     gemm(act_d_, L.self_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
-    launch_layernorm(dec_y_.get(), d, R, dr, d_, L.n2.g.get(), L.n2.b.get(), dec_a_.get(), d,
-                     stream_);
-    count();
-    prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    ln_dec(L.n2);
     gemm(act_d_, L.cross_q, R, dr, dec_cq_.get(), d, nullptr, nullptr, 0);
     launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
-                               enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d,
+                               enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d, od,
                                stream_);
     count();
-    prep(dec_ctx_.get(), d, d_, R, dr, nullptr, 0, act_d_);
     gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
-    launch_layernorm(dec_y_.get(), d, R, dr, d_, L.n3.g.get(), L.n3.b.get(), dec_a_.get(), d,
-                     stream_);
-    count();
-    prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+    ln_dec(L.n3);
     gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
     prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
     gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
   }
-  launch_layernorm(dec_y_.get(), d, R, dr, d_, dec_final_.g.get(), dec_final_.b.get(),
-                   dec_a_.get(), d, stream_);
-  count();
-  prep(dec_a_.get(), d, d_, R, dr, nullptr, 0, act_d_);
+  ln_dec(dec_final_);
   gemm(act_d_, logits_w_, R, dr, logits_.get(), Vp_, nullptr, nullptr, 0);
 }
 
@@ -669,7 +717,7 @@ void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double
     launch = [&, scale] {
       launch_dec_self_attention(qkv_cache_[0].get(), r_max_, T_, anc0_.get(), anc1_.get(),
                                 n_rows_.get(), step_.get(), d_, heads_, scale, dec_ctx_.get(), d_,
-                                stream_);
+                                opout(act_d_), stream_);
     };
     *bytes = 4.0 * R * (double(t + 1) * 2 * d_ + 2.0 * d_);
     *flops = 4.0 * R * (t + 1) * d_;

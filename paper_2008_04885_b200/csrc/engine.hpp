@@ -28,7 +28,8 @@ struct DevLinear {
   DeviceBuffer<int8_t> q;
   DeviceBuffer<__nv_bfloat16> h;
   DeviceBuffer<float> hi, lo;
-  DeviceBuffer<float> col_scale;  // int8: per-column weight scale
+  DeviceBuffer<float> seg_scale;  // int8: weight scale per fused segment
+  int seg_width = 0;              // columns per segment (0: one segment)
   Operand op() const;
 };
 
@@ -92,6 +93,10 @@ class Engine {
   void ensure_workspace(int n_sent, int m_enc, int beam);
   void prep(const float* x, long long ldx, int k, int max_rows, const int* d_rows,
             const int* seg_off, int n_seg, ActOperand& out);
+  OperandOut opout(ActOperand& a);
+  void prep_enc(const float* x, long long ldx, int k, int m, ActOperand& out, bool have_rowmax);
+  struct LN;
+  void ln_enc(const float* x, int m, const LN& ln, float* y, ActOperand& out);
   void gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
             long long ldc, const float* bias, const float* residual, int relu,
             long long c_step_stride = 0, const int* d_step = nullptr);
@@ -138,7 +143,8 @@ class Engine {
   std::vector<DeviceBuffer<float>> ckv_;
   DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;
   std::vector<DeviceBuffer<float>> qkv_cache_;
-  DeviceBuffer<int> src_ids_, src_pos_, src_off_, enc_off_, enc_len_;
+  DeviceBuffer<int> src_ids_, src_pos_, src_off_, enc_off_, enc_len_, src_rowseg_;
+  DeviceBuffer<float> rowmax_;  // per-row max |x| for int8 segment scales
   DeviceBuffer<int> nonfinite_;
   // beam state
   DeviceBuffer<int> step_, n_rows_, row_sent_, row_prev_, row_parent_, anc0_, anc1_, tok0_, tok1_,

@@ -3,6 +3,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -48,16 +49,15 @@ CUtensorMap make_map(const void* ptr, int prec, int rows, int k_pad, int box_row
 
 template <int PREC, int BN>
 void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
-  constexpr int smem = gemm_smem_bytes(PREC, BN);
   static bool configured = false;
   if (!configured) {
     MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
   dim3 grid(p.n_tiles, p.m_tiles);
-  gemm_tc_kernel<PREC, BN><<<grid, kGemmThreads, smem, stream>>>(p.a, p.b, p.a2, p.b2,
-                                                                 p.num_kb, ep);
+  gemm_tc_kernel<PREC, BN><<<grid, kGemmThreads, p.smem, stream>>>(p.a, p.b, p.a2, p.b2,
+                                                                   p.num_kb, p.nst, ep);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -95,6 +95,15 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   }
   p.bn = bn;
   p.n_tiles = (n + bn - 1) / bn;
+  // Pipeline depth: no deeper than the K loop, and shallow enough for two
+  // CTAs per SM when the tile allows it (epilogue / mainloop overlap).
+  const int stage = gemm_stage_bytes(a.prec, bn);
+  const int want = std::min(kMaxStages, std::max(2, p.num_kb));
+  const int two_per_sm = (113 * 1024 - kGemmSmemExtra) / stage;
+  const int one_per_sm = (227 * 1024 - kGemmSmemExtra) / stage;
+  p.nst = std::min(want, two_per_sm >= 2 ? two_per_sm : one_per_sm);
+  if (p.nst < 2 || p.nst * stage < kEpiStageBytes) fail(kStateError, "gemm: tile too large");
+  p.smem = p.nst * stage + kGemmSmemExtra;
   p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, bn);
   if (a.prec == kPrecTF32x3) {

@@ -32,6 +32,8 @@ struct GemmPlan {
   int num_kb = 0;
   int m_tiles = 0;
   int n_tiles = 0;
+  int nst = 0;   // pipeline stages
+  int smem = 0;  // dynamic shared memory bytes
 };
 
 // Plans C[M x N] = A[M x K] . B[N x K]^T for at most m_max rows of A.

@@ -2,9 +2,9 @@
 //
 // Both operands are K-major (row-major with K contiguous), staged by TMA with
 // 128-byte swizzle, one 128-byte K slab per pipeline stage. A single thread
-// issues tcgen05.mma into a TMEM accumulator (M = 128 lanes x BN columns); four
-// epilogue warps drain TMEM with tcgen05.ld and apply the fused epilogue of the
-// reference's linear layers:
+// issues tcgen05.mma into a TMEM accumulator (M = 128 lanes x BN columns);
+// eight epilogue warps drain TMEM with tcgen05.ld and apply the fused
+// epilogue of the reference's linear layers:
 //
 //   int8  (quant.cpp:155-193, model.cpp:461-466):
 //         v = float(acc_s32) * (1.0f / (sa[row] * sw[col]))
@@ -17,8 +17,10 @@
 // and accumulates A_lo.B_hi + A_hi.B_lo + A_hi.B_hi in fp32 TMEM, giving ~fp32
 // accuracy on the tensor pipe.
 //
-// Warp roles (192 threads): warp 0 = TMEM allocator + TMA producer, warp 1 =
-// MMA issuer, warps 2..5 = epilogue (warp w drains TMEM lanes 32*(w%4)..+31).
+// Warp roles (320 threads): warp 0 = TMEM allocator + TMA producer, warp 1 =
+// MMA issuer, warps 2..9 = epilogue (warp w drains TMEM lanes 32*(w%4)..+31,
+// column half (w-2)/4). The pipeline depth is a launch parameter so small-K
+// GEMMs run two CTAs per SM (one CTA's epilogue overlaps the other's MMAs).
 #pragma once
 
 #include <cstdint>
@@ -37,15 +39,20 @@ struct GemmEpilogue {
   const float* residual;     // [M x ldr] or null (may alias C)
   long long ldr;
   const float* a_scale;      // int8: per-row activation scale
-  const float* w_scale;      // int8: per-column weight scale
+  const float* w_seg_scale;  // int8: weight scale per column segment
+  int seg_width;             // columns per weight segment (fused q|k|v)
   int relu;
   int M;                     // rows, unless d_M != null
   const int* d_M;
   int N;
-  int vec;                   // 1: C/residual rows are 16-byte aligned (float4 path)
 };
 
 enum GemmPrec : int { kPrecI8 = 0, kPrecBF16 = 1, kPrecTF32x3 = 2 };
+
+constexpr int kMaxSegments = 4;
+constexpr int kMaxStages = 8;
+constexpr int kGemmThreads = 320;
+constexpr int kEpiWarps = 8;
 
 __host__ __device__ constexpr int prec_elem_bytes(int prec) {
   return prec == kPrecI8 ? 1 : prec == kPrecBF16 ? 2 : 4;
@@ -56,37 +63,29 @@ __host__ __device__ constexpr int prec_mma_kind(int prec) {
 __host__ __device__ constexpr int gemm_stage_bytes(int prec, int bn) {
   return (128 * 128 + bn * 128) * (prec == kPrecTF32x3 ? 2 : 1);
 }
-__host__ __device__ constexpr int gemm_stages(int prec, int bn) {
-  return (200 * 1024 / gemm_stage_bytes(prec, bn)) > 8
-             ? 8
-             : (200 * 1024 / gemm_stage_bytes(prec, bn));
-}
 __host__ __device__ constexpr int gemm_tmem_cols(int bn) {
   return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
 }
-__host__ __device__ constexpr int gemm_smem_bytes(int prec, int bn) {
-  return gemm_stages(prec, bn) * gemm_stage_bytes(prec, bn) + 1024 /*align*/ +
-         256 /*barriers*/;
-}
-
-constexpr int kGemmThreads = 192;
+constexpr int kGemmSmemExtra = 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kEpiStageBytes = kEpiWarps * 32 * 33 * 4;  // aliases the drained pipeline
 
 template <int PREC, int BN>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapA2,
-                   const __grid_constant__ CUtensorMap mapB2, int num_kb,
+                   const __grid_constant__ CUtensorMap mapB2, int num_kb, int nst,
                    GemmEpilogue ep) {
   constexpr bool kSplit = (PREC == kPrecTF32x3);
   constexpr int kKind = prec_mma_kind(PREC);
   constexpr int kElem = prec_elem_bytes(PREC);
   constexpr int kKbElems = 128 / kElem;      // K elements per 128-byte slab
-  constexpr int kStages = gemm_stages(PREC, BN);
   constexpr int kATile = 128 * 128;
   constexpr int kBTile = BN * 128;
   constexpr int kStageBytes = gemm_stage_bytes(PREC, BN);
   constexpr int kTmemCols = gemm_tmem_cols(BN);
+  constexpr int kHalf = BN / 2;                   // columns per epilogue warp
+  constexpr int kChunk = kHalf >= 32 ? 32 : 16;  // columns per TMEM load
 
   const int M = ep.d_M ? *ep.d_M : ep.M;
   const int m0 = blockIdx.y * 128;
@@ -96,9 +95,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* accum_bar = empty_bar + kStages;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * kStageBytes);
+  uint64_t* empty_bar = full_bar + kMaxStages;
+  uint64_t* accum_bar = empty_bar + kMaxStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -115,7 +114,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     tmem_alloc<kTmemCols>(tmem_slot);
   } else if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -131,9 +130,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       // ---- TMA producer ----
       for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (kb / kStages) & 1;
-        if (kb >= kStages) mbar_wait(&empty_bar[s], ph ^ 1);
+        const int s = kb % nst;
+        const uint32_t ph = (kb / nst) & 1;
+        if (kb >= nst) mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* st = smem + s * kStageBytes;
         mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
         tma_load_2d(st, &mapA, &full_bar[s], kb * kKbElems, m0);
@@ -150,8 +149,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ---- MMA issuer ----
       constexpr uint32_t idesc = make_idesc(kKind, 128, BN);
       for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (kb / kStages) & 1;
+        const int s = kb % nst;
+        const uint32_t ph = (kb / nst) & 1;
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
         const uint32_t a_base = smem_u32(smem + s * kStageBytes);
@@ -176,73 +175,83 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_commit(accum_bar);        // accumulator complete
     }
   } else {
-    // ---- epilogue: TMEM -> registers -> fused ops -> global ----
+    // ---- epilogue: TMEM -> registers -> smem transpose -> coalesced global ----
+    // Phase 1 (thread = row): convert a 32 x kChunk accumulator sub-tile
+    // (int8: x 1/(sa*sw), reciprocal hoisted per weight segment) into padded
+    // smem. Phase 2 (lane = column): bias / relu / residual and 128-byte
+    // coalesced row stores. The staging area aliases pipeline stage memory,
+    // which is drained once the accumulator barrier fires.
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    const bool row_ok = row < M;
+    const int half = (warp - 2) >> 2;
+    float* stage = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * 33);
+    const int rbase = m0 + q * 32;
+    const int nrows = min(32, M - rbase);  // warp-uniform, may be <= 0
+    float inv[kMaxSegments];
+    if constexpr (PREC == kPrecI8) {
+      const float sa = lane < nrows ? ep.a_scale[rbase + lane] : 1.0f;
+#pragma unroll
+      for (int s = 0; s < kMaxSegments; ++s) {
+        const int c0 = s * ep.seg_width;
+        inv[s] = c0 < ep.N ? __frcp_rn(__fmul_rn(sa, ep.w_seg_scale[s])) : 1.0f;
+      }
+    }
+    const long long step_off =
+        ep.d_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride : 0LL;
     mbar_wait(accum_bar, 0);
     tc_fence_after();
-
-    float* crow = ep.C + (ep.d_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride
-                                    : 0LL) +
-                  static_cast<long long>(row) * ep.ldc;
-    const float* rrow =
-        ep.residual ? ep.residual + static_cast<long long>(row) * ep.ldr : nullptr;
-    float sa = 1.0f;
-    if constexpr (PREC == kPrecI8) sa = row_ok ? ep.a_scale[row] : 1.0f;
-
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, r);
-      tmem_ld_wait();
-      const int col0 = n0 + c;
-      if (!row_ok || col0 >= ep.N) continue;
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if constexpr (PREC == kPrecI8) {
-          const int col = min(col0 + j, ep.N - 1);
-          const float inv = 1.0f / (sa * ep.w_scale[col]);
-          v[j] = __int2float_rn(static_cast<int>(r[j])) * inv;
-        } else {
-          v[j] = __uint_as_float(r[j]);
-        }
-      }
-      const bool full = ep.vec && (col0 + 16 <= ep.N);
-      if (ep.bias) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (full || col0 + j < ep.N) v[j] = v[j] + ep.bias[col0 + j];
-      }
-      if (ep.relu) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
-      }
-      if (rrow) {
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const float4 t = *reinterpret_cast<const float4*>(rrow + col0 + j);
-            v[j] = t.x + v[j];
-            v[j + 1] = t.y + v[j + 1];
-            v[j + 2] = t.z + v[j + 2];
-            v[j + 3] = t.w + v[j + 3];
-          }
-        } else {
-          for (int j = 0; j < 16; ++j)
-            if (col0 + j < ep.N) v[j] = rrow[col0 + j] + v[j];
-        }
-      }
-      if (full) {
-#pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4*>(crow + col0 + j) =
-              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    for (int c = half * kHalf; c < (half + 1) * kHalf; c += kChunk) {
+      uint32_t r[32];
+      if constexpr (kChunk == 32) {
+        tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, r);
       } else {
-        for (int j = 0; j < 16; ++j)
-          if (col0 + j < ep.N) crow[col0 + j] = v[j];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c,
+                  *reinterpret_cast<uint32_t(*)[16]>(r));
       }
+      tmem_ld_wait();
+      if (nrows <= 0 || n0 + c >= ep.N) continue;  // warp-uniform
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        float v;
+        if constexpr (PREC == kPrecI8) {
+          const int col = n0 + c + j;
+          const int seg = ep.seg_width > 0 ? min(col / ep.seg_width, kMaxSegments - 1) : 0;
+          float iv = inv[0];
+#pragma unroll
+          for (int s = 1; s < kMaxSegments; ++s) iv = seg == s ? inv[s] : iv;
+          v = __fmul_rn(__int2float_rn(static_cast<int>(r[j])), iv);
+        } else {
+          v = __uint_as_float(r[j]);
+        }
+        stage[lane * 33 + j] = v;
+      }
+      __syncwarp();
+      const int col = n0 + c + (lane % kChunk);
+      const bool col_ok = col < ep.N && lane < kChunk;
+      const float bias = (col_ok && ep.bias) ? ep.bias[col] : 0.0f;
+      // Residual loads of a row group are issued before its stores: C may
+      // alias the residual, so loads placed after stores would serialise.
+#pragma unroll 1
+      for (int i0 = 0; i0 < 32; i0 += 8) {
+        float res[8];
+        if (ep.residual) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            res[i] = (col_ok && i0 + i < nrows)
+                         ? ep.residual[static_cast<long long>(rbase + i0 + i) * ep.ldr + col]
+                         : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float v = stage[(i0 + i) * 33 + (lane % kChunk)];
+          if (ep.bias) v = __fadd_rn(v, bias);
+          if (ep.relu) v = v > 0.0f ? v : 0.0f;
+          if (ep.residual) v = __fadd_rn(res[i], v);
+          if (col_ok && i0 + i < nrows)
+            ep.C[step_off + static_cast<long long>(rbase + i0 + i) * ep.ldc + col] = v;
+        }
+      }
+      __syncwarp();
     }
   }
 

@@ -1,17 +1,53 @@
-#include "kernels.cuh"
-
+// Embedding, LayerNorm, segment quantization, attention and log-softmax/top-k
+// kernels. Pinned float orders: P1 lane-strided warp sums with
+// xor butterfly, P2 512-thread block sums, P3 sequential dot products,
+// context sums in key order, Cephes exp/log (detmath.cuh).
 #include <climits>
 
 #include "detmath.cuh"
 #include "errors.hpp"
+#include "kernels.cuh"
 
 namespace mtg {
 
 namespace {
 
 #define kNegInf (-__int_as_float(0x7f800000))
-constexpr int kBosIdDev = 2;  // model.hpp:18
-constexpr int kEosIdDev = 3;  // model.hpp:19
+
+// quant.cpp:113-118
+__device__ __forceinline__ int8_t quant1(float x, float scale) {
+  float v = roundf(__fmul_rn(x, scale));
+  v = fminf(127.0f, fmaxf(-127.0f, v));
+  return static_cast<int8_t>(v);
+}
+__device__ __forceinline__ float qscale_of(float max_abs) {
+  return max_abs == 0.0f ? 1.0f : __fdiv_rn(127.0f, max_abs);
+}
+
+// Writes row r of an operand from x[0..n) with `stride`-spaced workers
+// (a warp: lane/32, a CTA: tid/blockDim). scale is used for int8 only.
+__device__ __forceinline__ void write_operand(const OperandOut& o, long long r, const float* x,
+                                              int n, float scale, int tid, int stride) {
+  if (o.prec == 0) {
+    int8_t* q = o.q + r * o.k_pad;
+    for (int c = tid; c < o.k_pad; c += stride) q[c] = c < n ? quant1(x[c], scale) : 0;
+    if (tid == 0) o.row_scale[r] = scale;
+  } else if (o.prec == 1) {
+    __nv_bfloat16* h = o.h + r * o.k_pad;
+    for (int c = tid; c < o.k_pad; c += stride) h[c] = __float2bfloat16_rn(c < n ? x[c] : 0.0f);
+  } else {
+    float* hi = o.hi + r * o.k_pad;
+    float* lo = o.lo + r * o.k_pad;
+    for (int c = tid; c < o.k_pad; c += stride) {
+      const float v = c < n ? x[c] : 0.0f;
+      uint32_t hb;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+      const float hf = __uint_as_float(hb);
+      hi[c] = hf;
+      lo[c] = __fsub_rn(v, hf);
+    }
+  }
+}
 
 // ---- embeddings -------------------------------------------------------------------
 
@@ -44,12 +80,109 @@ __global__ void embed_tgt_kernel(const int* __restrict__ prev, const int* d_rows
   }
 }
 
-// ---- layer norm: one warp per row, P1 sums ------------------------------------------
+// ---- layer norm (P1 sums) ---------------------------------------------------------------
+
+// Row value c = lane + 32 i kept in registers (n <= 32*KPL): one pass over
+// HBM, no reload-after-store. Same P1 order as the generic kernel.
+template <int KPL>
+__global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx, int max_rows,
+                                     const int* d_rows, int n, const float* __restrict__ g,
+                                     const float* __restrict__ b, float* __restrict__ y,
+                                     long long ldy, float* __restrict__ rowmax, OperandOut op,
+                                     int has_op) {
+  const int rows = d_rows ? *d_rows : max_rows;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + r * ldx;
+  float xv[KPL], gv[KPL], bv[KPL];  // gain/bias loaded up front with x
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    xv[i] = c < n ? xr[c] : 0.0f;
+    gv[i] = c < n ? g[c] : 0.0f;
+    bv[i] = c < n ? b[c] : 0.0f;
+  }
+  float part = 0.0f;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i)
+    if (lane + 32 * i < n) part = __fadd_rn(part, xv[i]);
+  const float nf = static_cast<float>(n);
+  const float mu = __fdiv_rn(warp_allsum(part), nf);
+  float part2 = 0.0f;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i)
+    if (lane + 32 * i < n) {
+      const float dv = __fsub_rn(xv[i], mu);
+      part2 = __fadd_rn(part2, __fmul_rn(dv, dv));
+    }
+  const float var = __fdiv_rn(warp_allsum(part2), nf);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+  float mx = 0.0f;
+  int bad = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < n) {
+      xv[i] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[i], mu), inv), gv[i]), bv[i]);
+      mx = fmaxf(mx, fabsf(xv[i]));
+      bad |= !isfinite(xv[i]);
+    }
+  }
+  if (y) {
+    float* yr = y + r * ldy;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i)
+      if (lane + 32 * i < n) yr[lane + 32 * i] = xv[i];
+  }
+  mx = warp_allmax(mx);
+  if (rowmax && lane == 0) rowmax[r] = mx;
+  if (!has_op) return;
+  if (op.prec == 0) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(op.nonfinite, 1);
+    const float scale = qscale_of(mx);
+    int8_t* q = op.q + static_cast<long long>(r) * op.k_pad;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < op.k_pad) q[c] = c < n ? quant1(xv[i], scale) : 0;
+    }
+    for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) q[c] = 0;
+    if (lane == 0) op.row_scale[r] = scale;
+  } else if (op.prec == 1) {
+    __nv_bfloat16* h = op.h + static_cast<long long>(r) * op.k_pad;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < op.k_pad) h[c] = __float2bfloat16_rn(c < n ? xv[i] : 0.0f);
+    }
+    for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) h[c] = __float2bfloat16_rn(0.0f);
+  } else {
+    float* hi = op.hi + static_cast<long long>(r) * op.k_pad;
+    float* lo = op.lo + static_cast<long long>(r) * op.k_pad;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < op.k_pad) {
+        const float v = c < n ? xv[i] : 0.0f;
+        uint32_t hb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+        hi[c] = __uint_as_float(hb);
+        lo[c] = __fsub_rn(v, __uint_as_float(hb));
+      }
+    }
+    for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) {
+      hi[c] = 0.0f;
+      lo[c] = 0.0f;
+    }
+  }
+}
 
 __global__ void layernorm_kernel(const float* __restrict__ x, long long ldx, int max_rows,
                                  const int* d_rows, int n, const float* __restrict__ g,
                                  const float* __restrict__ b, float* __restrict__ y,
-                                 long long ldy) {
+                                 long long ldy, float* __restrict__ rowmax, OperandOut op,
+                                 int has_op) {
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -67,14 +200,61 @@ __global__ void layernorm_kernel(const float* __restrict__ x, long long ldx, int
   const float var = __fdiv_rn(warp_allsum(part2), nf);
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
   float* yr = y + r * ldy;
-  for (int c = lane; c < n; c += 32)
-    yr[c] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xr[c], mu), inv), g[c]), b[c]);
+  float mx = 0.0f;
+  int bad = 0;
+  for (int c = lane; c < n; c += 32) {
+    const float v = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xr[c], mu), inv), g[c]), b[c]);
+    yr[c] = v;
+    mx = fmaxf(mx, fabsf(v));
+    bad |= !isfinite(v);
+  }
+  mx = warp_allmax(mx);
+  if (rowmax && lane == 0) rowmax[r] = mx;
+  if (has_op) {
+    if (op.prec == 0 && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(op.nonfinite, 1);
+    __syncwarp();
+    write_operand(op, r, yr, n, qscale_of(mx), lane, 32);
+  }
 }
 
-// ---- attention -------------------------------------------------------------------------
+// ---- segment quantization ---------------------------------------------------------------
+
+__global__ void rowmax_kernel(const float* __restrict__ x, long long ldx, int rows, int n,
+                              float* __restrict__ rowmax, int* nonfinite) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + r * ldx;
+  float m = 0.0f;
+  int bad = 0;
+  for (int c = lane; c < n; c += 32) {
+    const float v = xr[c];
+    bad |= !isfinite(v);
+    m = fmaxf(m, fabsf(v));
+  }
+  m = warp_allmax(m);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+  if (lane == 0) rowmax[r] = m;
+}
+
+__global__ void quantize_seg_kernel(const float* __restrict__ x, long long ldx, int rows, int n,
+                                    const int* __restrict__ row_seg,
+                                    const int* __restrict__ seg_off,
+                                    const float* __restrict__ rowmax, OperandOut op) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int s = row_seg[r];
+  float m = 0.0f;
+  for (int i = seg_off[s] + lane; i < seg_off[s + 1]; i += 32) m = fmaxf(m, rowmax[i]);
+  m = warp_allmax(m);
+  write_operand(op, r, x + r * ldx, n, qscale_of(m), lane, 32);
+}
+
+// ---- attention ---------------------------------------------------------------------------
 
 // One query against n keys, one warp. q: dh floats in smem; s: n floats of
-// per-warp smem scratch. Orders: P3 dot, P1 sum, j-ascending context.
+// per-warp smem scratch. P3 dots, P1 sum, context summed in key order.
 template <class KP, class VP>
 __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float scale, KP kp,
                                             VP vp, float* s, float* out) {
@@ -101,17 +281,28 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
   mx = warp_allmax(mx);
   float part = 0.0f;
   for (int j = lane; j < n; j += 32) {
-    const float e = det_expf(__fsub_rn(s[j], mx));
+    const float e = det_expf_nonpos(__fsub_rn(s[j], mx));
     s[j] = e;
     part = __fadd_rn(part, e);
   }
   const float sum = warp_allsum(part);
   for (int j = lane; j < n; j += 32) s[j] = __fdiv_rn(s[j], sum);
   __syncwarp();
-  for (int c = lane; c < dh; c += 32) {
-    float acc = 0.0f;
-    for (int j = 0; j < n; ++j) acc = __fadd_rn(acc, __fmul_rn(s[j], vp(j)[c]));
-    out[c] = acc;
+  for (int c0 = 0; c0 < dh; c0 += 32) {
+    const int c = c0 + lane;
+    if (c < dh) {
+      float acc = 0.0f;
+      int j = 0;
+      for (; j + 4 <= n; j += 4) {
+        const float v0 = vp(j)[c], v1 = vp(j + 1)[c], v2 = vp(j + 2)[c], v3 = vp(j + 3)[c];
+        acc = __fadd_rn(acc, __fmul_rn(s[j], v0));
+        acc = __fadd_rn(acc, __fmul_rn(s[j + 1], v1));
+        acc = __fadd_rn(acc, __fmul_rn(s[j + 2], v2));
+        acc = __fadd_rn(acc, __fmul_rn(s[j + 3], v3));
+      }
+      for (; j < n; ++j) acc = __fadd_rn(acc, __fmul_rn(s[j], vp(j)[c]));
+      out[c] = acc;
+    }
   }
   __syncwarp();
 }
@@ -136,30 +327,63 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   }
 }
 
+// CTA epilogue shared by the decoder attention kernels: the context row sits
+// in smem (d floats, one slice per head-warp); write fp32 and the operand.
+__device__ __forceinline__ void finish_ctx_row(const float* row, int d, long long r, float* ctx,
+                                               long long ldc, const OperandOut& op, float* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  float m = 0.0f;
+  int bad = 0;
+  for (int c = tid; c < d; c += blockDim.x) {
+    const float v = row[c];
+    ctx[r * ldc + c] = v;
+    m = fmaxf(m, fabsf(v));
+    bad |= !isfinite(v);
+  }
+  m = warp_allmax(m);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) red[warp] = m;
+  if (bad && lane == 0 && op.prec == 0) atomicExch(op.nonfinite, 1);
+  __syncthreads();
+  if (warp == 0) {
+    float v = lane < nw ? red[lane] : 0.0f;
+    v = warp_allmax(v);
+    if (lane == 0) red[32] = v;
+  }
+  __syncthreads();
+  write_operand(op, r, row, d, qscale_of(red[32]), tid, blockDim.x);
+}
+
 __global__ void dec_self_attention_kernel(const float* __restrict__ cache, int r_max, int T,
                                           const int* __restrict__ anc0,
                                           const int* __restrict__ anc1, const int* d_rows,
                                           const int* d_step, int d, int dh, float scale,
-                                          float* __restrict__ ctx, long long ldc) {
+                                          float* __restrict__ ctx, long long ldc, OperandOut op) {
   extern __shared__ float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
   const int t = *d_step;
   const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int* ar = ((t & 1) ? anc1 : anc0) + static_cast<long long>(r) * T;
-  const long long ld3 = 3LL * d;
-  float* qs = sm + h * (dh + T);
+  float* row = sm;                                   // [d] context row
+  float* red = row + d;                              // [33]
+  int* arow = reinterpret_cast<int*>(red + 33);      // [T] ancestor rows
+  float* qs = reinterpret_cast<float*>(arow + T) + h * (dh + T);
   float* ss = qs + dh;
+  const int* ar = ((t & 1) ? anc1 : anc0) + static_cast<long long>(r) * T;
+  for (int j = threadIdx.x; j <= t; j += blockDim.x) arow[j] = ar[j];
+  const long long ld3 = 3LL * d;
   const float* q = cache + (static_cast<long long>(t) * r_max + r) * ld3 + h * dh;
   for (int c = lane; c < dh; c += 32) qs[c] = q[c];
-  __syncwarp();
+  __syncthreads();
   attend_warp(
       qs, t + 1, dh, scale,
-      [&](int j) { return cache + (static_cast<long long>(j) * r_max + ar[j]) * ld3 + d + h * dh; },
+      [&](int j) { return cache + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d + h * dh; },
       [&](int j) {
-        return cache + (static_cast<long long>(j) * r_max + ar[j]) * ld3 + 2 * d + h * dh;
+        return cache + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + 2 * d + h * dh;
       },
-      ss, ctx + r * ldc + h * dh);
+      ss, row + h * dh);
+  __syncthreads();
+  finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
 
 __global__ void dec_cross_attention_kernel(const float* __restrict__ cq, long long ldq,
@@ -168,7 +392,7 @@ __global__ void dec_cross_attention_kernel(const float* __restrict__ cq, long lo
                                            const int* __restrict__ enc_off,
                                            const int* __restrict__ enc_len, const int* d_rows,
                                            int max_src, int d, int dh, float scale,
-                                           float* __restrict__ ctx, long long ldc) {
+                                           float* __restrict__ ctx, long long ldc, OperandOut op) {
   extern __shared__ float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
@@ -176,324 +400,215 @@ __global__ void dec_cross_attention_kernel(const float* __restrict__ cq, long lo
   const int s = row_sent[r];
   const float* kv = ckv + static_cast<long long>(enc_off[s]) * 2 * d + h * dh;
   const int n = enc_len[s];
-  float* qs = sm + h * (dh + max_src);
+  float* row = sm;
+  float* red = row + d;
+  float* qs = red + 33 + h * (dh + max_src);
   float* ss = qs + dh;
   for (int c = lane; c < dh; c += 32) qs[c] = cq[r * ldq + h * dh + c];
   __syncwarp();
   attend_warp(
       qs, n, dh, scale, [&](int j) { return kv + static_cast<long long>(j) * 2 * d; },
-      [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; }, ss,
-      ctx + r * ldc + h * dh);
+      [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; }, ss, row + h * dh);
+  __syncthreads();
+  finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
 
-// ---- beam search ------------------------------------------------------------------------
+// ---- log-softmax + top-k -----------------------------------------------------------------
 
 __device__ __forceinline__ bool better2(float a, int ta, float b, int tb) {
   return a > b || (a == b && ta < tb);
 }
 
-// decode.cpp:64-69 total order: score desc, parent asc, token asc.
-__device__ __forceinline__ bool better3(float a, int pa, int ta, float b, int pb, int tb) {
-  if (a != b) return a > b;
-  if (pa != pb) return pa < pb;
-  return ta < tb;
-}
-
-__global__ void beam_init_kernel(BeamDev b) {
-  if (threadIdx.x != 0) return;
-  int base = 0;
-  for (int s = 0; s < b.N; ++s) {
-    b.best_has[s] = 0;
-    if (b.sent_done[s]) {
-      b.sent_live[s] = 0;
-      b.sent_row0[s] = base;
-      continue;
+// One 512-thread CTA per live row; thread t owns logits 4(t + 512 i) + c,
+// i < NV4, held in registers (one HBM pass). P2 sum order.
+// Block-wide argmax of (score desc, token asc) over one candidate per
+// thread; returns the winner in every thread. red_f/red_i: >= 32 entries.
+__device__ __forceinline__ void block_best(float& bs, int& bt, float* red_f, int* red_i) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kTopkThreads / 32;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+    const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ot != INT_MAX && (bt == INT_MAX || better2(os, ot, bs, bt))) {
+      bs = os;
+      bt = ot;
     }
-    b.sent_row0[s] = base;
-    b.sent_live[s] = 1;
-    b.row_sent[base] = s;
-    b.row_lp[base] = 0.0f;
-    b.row_prev[base] = kBosIdDev;
-    b.anc[0][static_cast<long long>(base) * b.T] = base;
-    ++base;
   }
-  *b.n_rows = base;
-  *b.step = 0;
+  __syncthreads();
+  if (lane == 0) {
+    red_f[warp] = bs;
+    red_i[warp] = bt;
+  }
+  __syncthreads();
+  bs = lane < kWarps ? red_f[lane] : kNegInf;
+  bt = lane < kWarps ? red_i[lane] : INT_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+    const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ot != INT_MAX && (bt == INT_MAX || better2(os, ot, bs, bt))) {
+      bs = os;
+      bt = ot;
+    }
+  }
 }
 
-// One CTA (1024 threads) per live row. P2 sum order.
-__global__ void __launch_bounds__(1024) topk_kernel(const float* __restrict__ logits,
-                                                    long long ldl, BeamDev b) {
+constexpr int kTopkListCap = 1024;
+
+// One 512-thread CTA per live row; thread t owns logits 4(t + 512 i) + c,
+// i < NV4, held in registers (one HBM pass). P2 sum order.
+//
+// Top-kB by (score desc, token asc), score = fl(parent + fl(x - lse)), exact:
+// tau = kB-th largest per-thread max is <= the kB-th largest logit, and score
+// is monotone in x, so every true top-kB element has score >= score(tau).
+// Those elements go to a shared list (normally ~kB entries) and are selected
+// exactly; rows whose list overflows (e.g. all-equal logits) take the exact
+// slow path over every element.
+template <int NV4>
+__global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restrict__ logits,
+                                                            long long ldl, BeamDev b) {
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;
   __shared__ float red_f[32];
   __shared__ int red_i[32];
-  __shared__ int red_o[32];
+  __shared__ float list_s[kTopkListCap];
+  __shared__ int list_t[kTopkListCap];
+  __shared__ int list_n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kTopkThreads / 32;
   const int V = b.V;
   const float* x = logits + r * ldl;
+  if (tid == 0) list_n = 0;
 
-  float mx = kNegInf;
-  for (int base = 4 * tid; base < V; base += 4096)
+  float v[NV4 * 4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (base + c < V) mx = fmaxf(mx, x[base + c]);
-  mx = warp_allmax(mx);
+  for (int i = 0; i < NV4; ++i) {
+    const int base = 4 * (tid + kTopkThreads * i);
+    if (base + 3 < V) {
+      const float4 f = *reinterpret_cast<const float4*>(x + base);
+      v[4 * i] = f.x;
+      v[4 * i + 1] = f.y;
+      v[4 * i + 2] = f.z;
+      v[4 * i + 3] = f.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[4 * i + c] = base + c < V ? x[base + c] : kNegInf;
+    }
+  }
+  float tmax = kNegInf;
+#pragma unroll
+  for (int i = 0; i < NV4 * 4; ++i) tmax = fmaxf(tmax, v[i]);
+  float mx = warp_allmax(tmax);
   if (lane == 0) red_f[warp] = mx;
   __syncthreads();
-  mx = warp_allmax(red_f[lane]);
+  mx = warp_allmax(lane < kWarps ? red_f[lane] : kNegInf);
   __syncthreads();
 
   float part = 0.0f;
-  for (int base = 4 * tid; base < V; base += 4096)
+#pragma unroll
+  for (int i = 0; i < NV4; ++i)
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (base + c < V) part = __fadd_rn(part, det_expf(__fsub_rn(x[base + c], mx)));
+      if (4 * (tid + kTopkThreads * i) + c < V)
+        part = __fadd_rn(part, det_expf_nonpos(__fsub_rn(v[4 * i + c], mx)));
   part = warp_allsum(part);
   if (lane == 0) red_f[warp] = part;
   __syncthreads();
-  const float total = warp_allsum(red_f[lane]);
+  const float total = warp_allsum(lane < kWarps ? red_f[lane] : 0.0f);
   const float lse = __fadd_rn(det_logf(total), mx);
   const float plp = b.row_lp[r];
-  __syncthreads();
-
   const int kB = min(b.B, V);
-  float sc[kMaxBeam];
-  int tk[kMaxBeam];
-  int cnt = 0;
-  for (int base = 4 * tid; base < V; base += 4096)
-    for (int c = 0; c < 4; ++c) {
-      const int j = base + c;
-      if (j >= V) break;
-      const float v = __fadd_rn(plp, __fsub_rn(x[j], lse));
-      if (cnt == kB && !better2(v, j, sc[kB - 1], tk[kB - 1])) continue;
-      int pos = cnt < kB ? cnt++ : kB - 1;
-      while (pos > 0 && better2(v, j, sc[pos - 1], tk[pos - 1])) {
-        sc[pos] = sc[pos - 1];
-        tk[pos] = tk[pos - 1];
-        --pos;
-      }
-      sc[pos] = v;
-      tk[pos] = j;
-    }
 
-  int head = 0;
-  for (int k = 0; k < kB; ++k) {
-    float bs = head < cnt ? sc[head] : kNegInf;
-    int bt = head < cnt ? tk[head] : INT_MAX;
-    int bo = head < cnt ? tid : -1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-      const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-      const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
-      if (oo >= 0 && (bo < 0 || better2(os, ot, bs, bt))) {
-        bs = os;
-        bt = ot;
-        bo = oo;
+  // tau: kB-th largest per-thread max (thread index breaks value ties).
+  // Fewer than kB threads holding logits: no bound, keep everything.
+  float tau = kNegInf;
+  {
+    float mine = tmax;
+    for (int k = 0; k < kB; ++k) {
+      float bs = mine;
+      int bt = mine == kNegInf ? INT_MAX : tid;
+      block_best(bs, bt, red_f, red_i);  // larger value first, lower tid on ties
+      if (bt == INT_MAX) {
+        tau = kNegInf;
+        break;
       }
+      tau = bs;
+      if (bt == tid) mine = kNegInf;
     }
-    if (lane == 0) {
-      red_f[warp] = bs;
-      red_i[warp] = bt;
-      red_o[warp] = bo;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      bs = red_f[lane];
-      bt = red_i[lane];
-      bo = red_o[lane];
+  }
+  const float s_lb = tau == kNegInf ? kNegInf : __fadd_rn(plp, __fsub_rn(tau, lse));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-        const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-        const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
-        if (oo >= 0 && (bo < 0 || better2(os, ot, bs, bt))) {
-          bs = os;
-          bt = ot;
-          bo = oo;
+  for (int i = 0; i < NV4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = 4 * (tid + kTopkThreads * i) + c;
+      if (j < V) {
+        const float sc = __fadd_rn(plp, __fsub_rn(v[4 * i + c], lse));
+        if (sc >= s_lb) {
+          const int slot = atomicAdd(&list_n, 1);
+          if (slot < kTopkListCap) {
+            list_s[slot] = sc;
+            list_t[slot] = j;
+          }
         }
       }
-      if (lane == 0) {
+    }
+  __syncthreads();
+  const int n_list = list_n;
+
+  if (n_list <= kTopkListCap) {
+    unsigned taken = 0u;  // entries tid + 512 e, e < 2
+    for (int k = 0; k < kB; ++k) {
+      float bs = kNegInf;
+      int bt = INT_MAX;
+#pragma unroll
+      for (int e = 0; e < kTopkListCap / kTopkThreads; ++e) {
+        const int idx = tid + kTopkThreads * e;
+        if (idx < n_list && !((taken >> e) & 1u) &&
+            (bt == INT_MAX || better2(list_s[idx], list_t[idx], bs, bt))) {
+          bs = list_s[idx];
+          bt = list_t[idx];
+        }
+      }
+      block_best(bs, bt, red_f, red_i);
+      if (tid == 0) {
         b.cand_score[static_cast<long long>(r) * b.B + k] = bs;
         b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
-        red_o[0] = bo;
-      }
-    }
-    __syncthreads();
-    if (red_o[0] == tid) ++head;
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(1024) beam_select_kernel(BeamDev b) {
-  const int t = *b.step;
-  const int cur = t & 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kB = min(b.B, b.V);
-  const int T = b.T;
-  __shared__ uint32_t taken_all[32][kMaxBeam * kMaxBeam / 32];
-  uint32_t* taken = taken_all[warp];
-  const int* tok_cur = b.tok[cur];
-
-  for (int s = warp; s < b.N; s += 32) {
-    if (b.sent_done[s]) continue;
-    const int L = b.sent_live[s], r0 = b.sent_row0[s];
-    const int nc = L * kB;
-    for (int w = lane; w < kMaxBeam * kMaxBeam / 32; w += 32) taken[w] = 0;
-    __syncwarp();
-    const int n_sel = min(b.B, nc);
-    int q = 0;
-    for (int k = 0; k < n_sel; ++k) {
-      float bs = kNegInf;
-      int bp = INT_MAX, bt = INT_MAX, bc = -1;
-      for (int c = lane; c < nc; c += 32) {
-        if (taken[c >> 5] & (1u << (c & 31))) continue;
-        const int p = c / kB, e = c % kB;
-        const long long idx = static_cast<long long>(r0 + p) * b.B + e;
-        const float sc = b.cand_score[idx];
-        const int tk = b.cand_tok[idx];
-        if (bc < 0 || better3(sc, p, tk, bs, bp, bt)) {
-          bs = sc;
-          bp = p;
-          bt = tk;
-          bc = c;
-        }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (oc >= 0 && (bc < 0 || better3(os, op, ot, bs, bp, bt))) {
-          bs = os;
-          bp = op;
-          bt = ot;
-          bc = oc;
-        }
+      for (int e = 0; e < kTopkListCap / kTopkThreads; ++e) {
+        const int idx = tid + kTopkThreads * e;
+        if (idx < n_list && list_t[idx] == bt) taken |= 1u << e;
       }
-      if (lane == 0) taken[bc >> 5] |= 1u << (bc & 31);
-      const int pr = r0 + bp;
-      if (bt == kEosIdDev) {
-        // decode.cpp:77-80 + first max of normalized_score over finished.
-        const float len = static_cast<float>(t) + 1.0f;
-        const float norm = __fdiv_rn(bs, det_powf(__fdiv_rn(__fadd_rn(5.0f, len), 6.0f), b.alpha));
-        const bool repl = !b.best_has[s] || norm > b.best_norm[s];
-        __syncwarp();
-        if (repl) {
-          for (int j = lane; j < t; j += 32)
-            b.best_tok[static_cast<long long>(s) * T + j] = tok_cur[static_cast<long long>(pr) * T + j];
-          if (lane == 0) {
-            b.best_has[s] = 1;
-            b.best_norm[s] = norm;
-            b.best_lp[s] = bs;
-            b.best_len[s] = t;
+    }
+    return;
+  }
+
+  // Slow exact path: kB rounds over every element with a taken mask.
+  unsigned long long taken = 0ull;
+  for (int k = 0; k < kB; ++k) {
+    float bs = kNegInf;
+    int bt = INT_MAX;
+#pragma unroll
+    for (int i = 0; i < NV4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = 4 * (tid + kTopkThreads * i) + c;
+        if (j < V && !((taken >> (4 * i + c)) & 1ull)) {
+          const float sc = __fadd_rn(plp, __fsub_rn(v[4 * i + c], lse));
+          if (bt == INT_MAX || better2(sc, j, bs, bt)) {
+            bs = sc;
+            bt = j;
           }
         }
-      } else {
-        if (lane == 0) {
-          b.sel_parent[s * b.B + q] = pr;
-          b.sel_tok[s * b.B + q] = bt;
-          b.sel_lp[s * b.B + q] = bs;
-        }
-        ++q;
       }
-      __syncwarp();
+    block_best(bs, bt, red_f, red_i);
+    if (tid == 0) {
+      b.cand_score[static_cast<long long>(r) * b.B + k] = bs;
+      b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
     }
-
-    int new_live = q;
-    if (new_live > 0 && t + 1 >= b.max_seq_len && b.sent_maxlen[s] > b.max_seq_len) {
-      // decode_step would be called past max_seq_len (model.cpp:618-619).
-      if (lane == 0) {
-        b.res_status[s] = 2;  // ValueError
-        b.res_flags[s] = 4u;
-        b.res_len[s] = 0;
-        b.sent_done[s] = 1;
-      }
-      new_live = 0;
-    } else if (new_live == 0 || t + 1 >= b.sent_maxlen[s]) {
-      if (b.best_has[s]) {  // decode.cpp:89-98
-        const int n = b.best_len[s];
-        for (int j = lane; j < n; j += 32)
-          b.res_tok[static_cast<long long>(s) * T + j] = b.best_tok[static_cast<long long>(s) * T + j];
-        if (lane == 0) {
-          b.res_len[s] = n;
-          b.res_lp[s] = b.best_lp[s];
-          b.res_norm[s] = b.best_norm[s];
-          b.res_flags[s] = 1u;
-        }
-      } else {  // decode.cpp:99-108: first max over live, truncated
-        const float len = static_cast<float>(t + 1) + 1.0f;
-        const float den = det_powf(__fdiv_rn(__fadd_rn(5.0f, len), 6.0f), b.alpha);
-        int bq = 0;
-        float bn = __fdiv_rn(b.sel_lp[s * b.B], den);
-        for (int qq = 1; qq < new_live; ++qq) {
-          const float nq = __fdiv_rn(b.sel_lp[s * b.B + qq], den);
-          if (nq > bn) {
-            bn = nq;
-            bq = qq;
-          }
-        }
-        const int pr = b.sel_parent[s * b.B + bq];
-        for (int j = lane; j < t; j += 32)
-          b.res_tok[static_cast<long long>(s) * T + j] = tok_cur[static_cast<long long>(pr) * T + j];
-        if (lane == 0) {
-          b.res_tok[static_cast<long long>(s) * T + t] = b.sel_tok[s * b.B + bq];
-          b.res_len[s] = t + 1;
-          b.res_lp[s] = b.sel_lp[s * b.B + bq];
-          b.res_norm[s] = bn;
-          b.res_flags[s] = 2u;
-        }
-      }
-      if (lane == 0) {
-        b.res_status[s] = 0;
-        b.sent_done[s] = 1;
-      }
-      new_live = 0;
-    }
-    if (lane == 0) b.sent_live[s] = new_live;
-    __syncwarp();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int base = 0;
-    for (int s = 0; s < b.N; ++s) {
-      b.sent_row0[s] = base;
-      base += b.sent_live[s];
-    }
-    *b.n_rows = base;
-  }
-  __syncthreads();
-  for (int s = warp; s < b.N; s += 32) {
-    const int L = b.sent_live[s];
-    for (int q = lane; q < L; q += 32) {
-      const int row = b.sent_row0[s] + q;
-      b.row_sent[row] = s;
-      b.row_parent[row] = b.sel_parent[s * b.B + q];
-      b.row_prev[row] = b.sel_tok[s * b.B + q];
-      b.row_lp[row] = b.sel_lp[s * b.B + q];
-    }
-  }
-  if (threadIdx.x == 0) *b.step = t + 1;
-}
-
-__global__ void beam_reorder_kernel(BeamDev b) {
-  const int r = blockIdx.x;
-  if (r >= *b.n_rows) return;
-  const int tn = *b.step;
-  const int cur = (tn - 1) & 1, nxt = tn & 1;
-  const int T = b.T;
-  const int pr = b.row_parent[r];
-  const int* ac = b.anc[cur] + static_cast<long long>(pr) * T;
-  int* an = b.anc[nxt] + static_cast<long long>(r) * T;
-  const int* tc = b.tok[cur] + static_cast<long long>(pr) * T;
-  int* tnw = b.tok[nxt] + static_cast<long long>(r) * T;
-  for (int j = threadIdx.x; j < tn && j < T; j += blockDim.x) an[j] = ac[j];
-  for (int j = threadIdx.x; j < tn - 1; j += blockDim.x) tnw[j] = tc[j];
-  if (threadIdx.x == 0) {
-    if (tn < T) an[tn] = r;
-    if (tn - 1 < T) tnw[tn - 1] = b.row_prev[r];
+    if (((bt >> 2) % kTopkThreads) == tid) taken |= 1ull << (4 * ((bt >> 2) / kTopkThreads) + (bt & 3));
   }
 }
 
@@ -518,11 +633,44 @@ void launch_embed_tgt(const int* prev, const int* d_rows, int max_rows, const in
 }
 
 void launch_layernorm(const float* x, long long ldx, int max_rows, const int* d_rows, int n,
-                      const float* g, const float* b, float* y, long long ldy, cudaStream_t st) {
+                      const float* g, const float* b, float* y, long long ldy, float* rowmax,
+                      const OperandOut* op, cudaStream_t st) {
   if (max_rows <= 0) return;
+  const int wpb = 4;
+  const dim3 grid((max_rows + wpb - 1) / wpb), block(wpb * 32);
+  const OperandOut o = op ? *op : OperandOut{};
+  const int has = op ? 1 : 0;
+  const int kpl = (n + 31) / 32;
+  if (kpl <= 1)
+    layernorm_reg_kernel<1><<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy,
+                                                     rowmax, o, has);
+  else if (kpl <= 4)
+    layernorm_reg_kernel<4><<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy,
+                                                     rowmax, o, has);
+  else if (kpl <= 16)
+    layernorm_reg_kernel<16><<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy,
+                                                      rowmax, o, has);
+  else
+    layernorm_kernel<<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy, rowmax, o,
+                                             has);
+  MTG_CUDA(cudaGetLastError());
+}
+
+void launch_rowmax(const float* x, long long ldx, int rows, int n, float* rowmax, int* nonfinite,
+                   cudaStream_t st) {
+  if (rows <= 0) return;
   const int wpb = 8;
-  layernorm_kernel<<<(max_rows + wpb - 1) / wpb, wpb * 32, 0, st>>>(x, ldx, max_rows, d_rows, n,
-                                                                    g, b, y, ldy);
+  rowmax_kernel<<<(rows + wpb - 1) / wpb, wpb * 32, 0, st>>>(x, ldx, rows, n, rowmax, nonfinite);
+  MTG_CUDA(cudaGetLastError());
+}
+
+void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const int* row_seg,
+                         const int* seg_off, const float* rowmax, const OperandOut& op,
+                         cudaStream_t st) {
+  if (rows <= 0) return;
+  const int wpb = 8;
+  quantize_seg_kernel<<<(rows + wpb - 1) / wpb, wpb * 32, 0, st>>>(x, ldx, rows, n, row_seg,
+                                                                   seg_off, rowmax, op);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -541,45 +689,52 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
 void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const int* anc0,
                                const int* anc1, const int* d_rows, const int* d_step, int d,
                                int heads, float scale, float* ctx, long long ldc,
-                               cudaStream_t st) {
+                               const OperandOut& op, cudaStream_t st) {
   if (r_max <= 0) return;
   const int dh = d / heads;
-  const size_t smem = sizeof(float) * heads * (dh + T);
+  const size_t smem = sizeof(float) * (d + 33 + T + heads * (dh + T));
   dec_self_attention_kernel<<<r_max, heads * 32, smem, st>>>(qkv_cache, r_max, T, anc0, anc1,
                                                              d_rows, d_step, d, dh, scale, ctx,
-                                                             ldc);
+                                                             ldc, op);
   MTG_CUDA(cudaGetLastError());
 }
 
 void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv,
                                 const int* row_sent, const int* enc_off, const int* enc_len,
                                 const int* d_rows, int max_rows, int max_src, int d, int heads,
-                                float scale, float* ctx, long long ldc, cudaStream_t st) {
+                                float scale, float* ctx, long long ldc, const OperandOut& op,
+                                cudaStream_t st) {
   if (max_rows <= 0) return;
   const int dh = d / heads;
-  const size_t smem = sizeof(float) * heads * (dh + max_src);
+  const size_t smem = sizeof(float) * (d + 33 + heads * (dh + max_src));
   dec_cross_attention_kernel<<<max_rows, heads * 32, smem, st>>>(
-      cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows, max_src, d, dh, scale, ctx, ldc);
+      cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows, max_src, d, dh, scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
 }
 
-void launch_beam_init(const BeamDev& b, cudaStream_t st) {
-  beam_init_kernel<<<1, 32, 0, st>>>(b);
-  MTG_CUDA(cudaGetLastError());
+template <int NV4>
+static void launch_topk_nv(const float* logits, long long ldl, const BeamDev& b,
+                           cudaStream_t st) {
+  topk_kernel<NV4><<<b.R_max, kTopkThreads, 0, st>>>(logits, ldl, b);
 }
 
 void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st) {
-  topk_kernel<<<b.R_max, 1024, 0, st>>>(logits, ldl, b);
-  MTG_CUDA(cudaGetLastError());
-}
-
-void launch_beam_select(const BeamDev& b, cudaStream_t st) {
-  beam_select_kernel<<<1, 1024, 0, st>>>(b);
-  MTG_CUDA(cudaGetLastError());
-}
-
-void launch_beam_reorder(const BeamDev& b, cudaStream_t st) {
-  beam_reorder_kernel<<<b.R_max, 128, 0, st>>>(b);
+  const int per = 4 * kTopkThreads;
+  const int nv4 = (b.V + per - 1) / per;
+  if (ldl % 4 != 0) fail(kStateError, "topk: logits pitch must be a multiple of 4");
+  if (b.B > kMaxBeam) fail(kUsageError, "beam size above 16 is not supported");
+  if (nv4 <= 1)
+    launch_topk_nv<1>(logits, ldl, b, st);
+  else if (nv4 <= 2)
+    launch_topk_nv<2>(logits, ldl, b, st);
+  else if (nv4 <= 4)
+    launch_topk_nv<4>(logits, ldl, b, st);
+  else if (nv4 <= 8)
+    launch_topk_nv<8>(logits, ldl, b, st);
+  else if (nv4 <= 16)
+    launch_topk_nv<16>(logits, ldl, b, st);
+  else
+    fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
   MTG_CUDA(cudaGetLastError());
 }
 

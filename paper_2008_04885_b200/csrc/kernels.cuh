@@ -3,11 +3,27 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace mtg {
 
 constexpr int kMaxBeam = 16;
+constexpr int kTopkThreads = 512;
+
+// Destination of a row's GEMM operand (the next linear layer's A matrix):
+// int8 + per-row scale (quant.cpp:108-122), bf16, or fp32 hi/lo (3xTF32).
+// prec uses the GemmPrec numbering (0 = int8, 1 = bf16, 2 = tf32x3).
+struct OperandOut {
+  int prec = 0;
+  int k_pad = 0;
+  int8_t* q = nullptr;
+  float* row_scale = nullptr;
+  __nv_bfloat16* h = nullptr;
+  float* hi = nullptr;
+  float* lo = nullptr;
+  int* nonfinite = nullptr;
+};
 
 // ---- embeddings (model.cpp:539-581, 624-626) -----------------------------------
 
@@ -23,8 +39,21 @@ void launch_embed_tgt(const int* prev, const int* d_rows, int max_rows, const in
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st);
 
 // ---- layer norm (tensor.cpp:368-387) -------------------------------------------
+// One warp per row. Optional outputs: y (fp32), rowmax (max |y| per row, for
+// segment quantization), op (the row's GEMM operand; only valid when the
+// quantization segment is the row itself or the precision is not int8).
 void launch_layernorm(const float* x, long long ldx, int max_rows, const int* d_rows, int n,
-                      const float* g, const float* b, float* y, long long ldy, cudaStream_t st);
+                      const float* g, const float* b, float* y, long long ldy, float* rowmax,
+                      const OperandOut* op, cudaStream_t st);
+
+// ---- int8 segment quantization (quant.cpp:108-122) ----------------
+void launch_rowmax(const float* x, long long ldx, int rows, int n, float* rowmax, int* nonfinite,
+                   cudaStream_t st);
+// Row r belongs to segment row_seg[r] = rows [seg_off[s], seg_off[s+1]); its
+// scale is 127 / max(rowmax over the segment).
+void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const int* row_seg,
+                         const int* seg_off, const float* rowmax, const OperandOut& op,
+                         cudaStream_t st);
 
 // ---- attention (model.cpp:509-528, 642-665) ------------------------------------
 
@@ -37,17 +66,19 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
 // Decoder self-attention for live row r at step t over positions 0..t; the key
 // of position j lives in row anc[r*T + j] of the step-j slab of qkv_cache
 // ([T][R_max][3d]). anc0/anc1: the double-buffered ancestor tables (t & 1).
+// The context row is written as fp32 (ctx) and as the next GEMM's operand.
 void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const int* anc0,
                                const int* anc1, const int* d_rows, const int* d_step, int d,
                                int heads, float scale, float* ctx, long long ldc,
-                               cudaStream_t st);
+                               const OperandOut& op, cudaStream_t st);
 
 // Decoder cross-attention: row r attends to its sentence's encoder rows
 // (enc_off[s]..+enc_len[s]) in ckv ([M_enc][2d] = [k | v]).
 void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv,
                                 const int* row_sent, const int* enc_off, const int* enc_len,
                                 const int* d_rows, int max_rows, int max_src, int d, int heads,
-                                float scale, float* ctx, long long ldc, cudaStream_t st);
+                                float scale, float* ctx, long long ldc, const OperandOut& op,
+                                cudaStream_t st);
 
 // ---- beam search (decode.cpp:25-109) -------------------------------------------
 
@@ -89,7 +120,8 @@ struct BeamDev {
 void launch_beam_init(const BeamDev& b, cudaStream_t st);
 
 // log_softmax_row + candidate scores + per-row top-min(B,V) by (score desc,
-// token asc); one 1024-thread CTA per live row.
+// token asc); one 512-thread CTA per live row, logits held in registers.
+// Supports V <= 32768.
 void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st);
 
 // Per-sentence selection of beam_size candidates by (score desc, parent asc,

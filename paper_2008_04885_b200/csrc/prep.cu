@@ -89,6 +89,40 @@ __global__ void quantize_rows_kernel(const float* __restrict__ x, long long ld_x
   if (lane == 0) row_scale[r] = scale;
 }
 
+// Register-resident variant (k <= 32*KPL): the row is read once.
+template <int KPL>
+__global__ void quantize_rows_reg_kernel(const float* __restrict__ x, long long ld_x, int k,
+                                         int max_rows, const int* d_rows,
+                                         int8_t* __restrict__ q, int k_pad,
+                                         float* __restrict__ row_scale, int* nonfinite) {
+  const int rows = d_rows ? *d_rows : max_rows;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + r * ld_x;
+  float v[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) v[i] = lane + 32 * i < k ? xr[lane + 32 * i] : 0.0f;
+  float m = 0.0f;
+  int bad = 0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    bad |= !isfinite(v[i]);
+    m = fmaxf(m, fabsf(v[i]));
+  }
+  m = warp_max(m);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+  const float scale = scale_of(m);
+  int8_t* qr = q + static_cast<long long>(r) * k_pad;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < k_pad) qr[c] = c < k ? quant1(v[i], scale) : 0;
+  }
+  for (int c = 32 * KPL + lane; c < k_pad; c += 32) qr[c] = 0;
+  if (lane == 0) row_scale[r] = scale;
+}
+
 __global__ void cast_bf16_kernel(const float* __restrict__ x, long long ld_x, int k,
                                  int max_rows, const int* d_rows,
                                  __nv_bfloat16* __restrict__ out, int k_pad) {
@@ -133,8 +167,17 @@ void launch_quantize_rows(const float* x, long long ld_x, int k, int max_rows,
                           int* nonfinite_flag, cudaStream_t st) {
   if (max_rows <= 0) return;
   const int wpb = 8;
-  quantize_rows_kernel<<<(max_rows + wpb - 1) / wpb, wpb * 32, 0, st>>>(
-      x, ld_x, k, max_rows, d_rows, q, k_pad, row_scale, nonfinite_flag);
+  const dim3 grid((max_rows + wpb - 1) / wpb), block(wpb * 32);
+  const int kpl = (k + 31) / 32;
+  if (kpl <= 16)
+    quantize_rows_reg_kernel<16><<<grid, block, 0, st>>>(x, ld_x, k, max_rows, d_rows, q, k_pad,
+                                                         row_scale, nonfinite_flag);
+  else if (kpl <= 64)
+    quantize_rows_reg_kernel<64><<<grid, block, 0, st>>>(x, ld_x, k, max_rows, d_rows, q, k_pad,
+                                                         row_scale, nonfinite_flag);
+  else
+    quantize_rows_kernel<<<grid, block, 0, st>>>(x, ld_x, k, max_rows, d_rows, q, k_pad,
+                                                 row_scale, nonfinite_flag);
   MTG_CUDA(cudaGetLastError());
 }
 
