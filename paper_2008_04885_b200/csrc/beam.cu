@@ -4,6 +4,7 @@
 
 #include "detmath.cuh"
 #include "errors.hpp"
+#include "launch.cuh"
 #include "kernels.cuh"
 
 namespace mtg {
@@ -24,6 +25,8 @@ __device__ __forceinline__ bool better3(float a, int pa, int ta, float b, int pb
 }
 
 __global__ void beam_init_kernel(BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0) return;
   int base = 0;
   for (int s = 0; s < b.N; ++s) {
@@ -46,6 +49,8 @@ __global__ void beam_init_kernel(BeamDev b) {
 }
 
 __global__ void __launch_bounds__(1024) beam_select_kernel(BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
   const int t = *b.step;
   const int cur = t & 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -214,6 +219,8 @@ __global__ void __launch_bounds__(1024) beam_select_kernel(BeamDev b) {
 }
 
 __global__ void beam_reorder_kernel(BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;
   const int tn = *b.step;
@@ -235,17 +242,17 @@ __global__ void beam_reorder_kernel(BeamDev b) {
 }  // namespace
 
 void launch_beam_init(const BeamDev& b, cudaStream_t st) {
-  beam_init_kernel<<<1, 32, 0, st>>>(b);
+  launch_k(beam_init_kernel, 1, 32, 0, st, b);
   MTG_CUDA(cudaGetLastError());
 }
 
 void launch_beam_select(const BeamDev& b, cudaStream_t st) {
-  beam_select_kernel<<<1, 1024, 0, st>>>(b);
+  launch_k(beam_select_kernel, 1, 1024, 0, st, b);
   MTG_CUDA(cudaGetLastError());
 }
 
 void launch_beam_reorder(const BeamDev& b, cudaStream_t st) {
-  beam_reorder_kernel<<<b.R_max, 128, 0, st>>>(b);
+  launch_k(beam_reorder_kernel, b.R_max, 128, 0, st, b);
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -177,6 +177,8 @@ Engine::Engine(HostModel model, int precision, int device)
 Engine::~Engine() {
   cudaSetDevice(device_);
   plan_cache(this).clear();
+  if (step_exec_) cudaGraphExecDestroy(step_exec_);
+  if (step_graph_) cudaGraphDestroy(step_graph_);
   if (h_pinned_) cudaFreeHost(h_pinned_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -253,6 +255,7 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   cap_enc_ = std::max(m_enc, cap_enc_);
   cap_beam_ = std::max(beam, cap_beam_);
   plan_cache(this).clear();
+  ++ws_gen_;
   const ModelConfig& c = host_.config;
   const int N = cap_sent_, M = cap_enc_, B = cap_beam_;
   r_max_ = N * B;
@@ -575,15 +578,45 @@ void Engine::decoder_body() {
   gemm(act_d_, logits_w_, R, dr, logits_.get(), Vp_, nullptr, nullptr, 0);
 }
 
-void Engine::decode_loop(int t_run) {
-  launch_beam_init(beam_, stream_);
-  count();
-  for (int t = 0; t < t_run; ++t) {
+void Engine::ensure_step_graph() {
+  StepKey key;
+  key.n = beam_.N;
+  key.b = beam_.B;
+  key.r_max = r_max_;
+  key.gen = ws_gen_;
+  key.alpha = beam_.alpha;
+  if (step_exec_ && key == step_key_) return;
+  if (step_exec_) cudaGraphExecDestroy(step_exec_);
+  if (step_graph_) cudaGraphDestroy(step_graph_);
+  step_exec_ = nullptr;
+  step_graph_ = nullptr;
+  const int64_t before = launches_;
+  MTG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  try {
     decoder_body();
     launch_topk(logits_.get(), Vp_, beam_, stream_);
     launch_beam_select(beam_, stream_);
     launch_beam_reorder(beam_, stream_);
-    launches_ += 3;
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  MTG_CUDA(cudaStreamEndCapture(stream_, &step_graph_));
+  MTG_CUDA(cudaGraphInstantiate(&step_exec_, step_graph_, 0));
+  step_kernels_ = launches_ - before + 3;
+  launches_ = before;
+  step_key_ = key;
+}
+
+void Engine::decode_loop(int t_run) {
+  launch_beam_init(beam_, stream_);
+  count();
+  ensure_step_graph();
+  for (int t = 0; t < t_run; ++t) {
+    MTG_CUDA(cudaGraphLaunch(step_exec_, stream_));
+    launches_ += step_kernels_;
     if ((t + 1) % 8 == 0 && t + 1 < t_run) {
       MTG_CUDA(cudaMemcpyAsync(h_pinned_, n_rows_.get(), sizeof(int), cudaMemcpyDeviceToHost,
                                stream_));

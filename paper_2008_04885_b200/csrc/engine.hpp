@@ -161,6 +161,21 @@ class Engine {
   std::vector<int> staged_status_;
   int last_beam_ = 0, last_t_run_ = 0;
   DeviceBuffer<int> scratch_rows_;  // fixed row count for kernel timing
+
+  // One decode step (decoder layers, logits, top-k, beam bookkeeping) as a
+  // CUDA graph, re-captured when the batch shape / beam / alpha changes.
+  void ensure_step_graph();
+  cudaGraph_t step_graph_ = nullptr;
+  cudaGraphExec_t step_exec_ = nullptr;
+  int64_t step_kernels_ = 0;
+  int ws_gen_ = 0;
+  struct StepKey {
+    int n = -1, b = -1, r_max = -1, gen = -1;
+    float alpha = 0.0f;
+    bool operator==(const StepKey& o) const {
+      return n == o.n && b == o.b && r_max == o.r_max && gen == o.gen && alpha == o.alpha;
+    }
+  } step_key_;
 };
 
 }  // namespace mtg

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "errors.hpp"
+#include "launch.cuh"
 
 namespace mtg {
 
@@ -56,7 +57,7 @@ void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) 
     configured = true;
   }
   dim3 grid(p.n_tiles, p.m_tiles);
-  gemm_tc_kernel<PREC, BN><<<grid, kGemmThreads, p.smem, stream>>>(p.a, p.b, p.a2, p.b2,
+  launch_k(gemm_tc_kernel<PREC, BN>, grid, kGemmThreads, p.smem, stream, p.a, p.b, p.a2, p.b2,
                                                                    p.num_kb, p.nst, ep);
   MTG_CUDA(cudaGetLastError());
 }

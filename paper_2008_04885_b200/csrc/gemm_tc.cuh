@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <cuda.h>
 
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace mtg {
@@ -87,9 +88,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   constexpr int kHalf = BN / 2;                   // columns per epilogue warp
   constexpr int kChunk = kHalf >= 32 ? 32 : 16;  // columns per TMEM load
 
-  const int M = ep.d_M ? *ep.d_M : ep.M;
   const int m0 = blockIdx.y * 128;
-  if (m0 >= M) return;  // uniform across the CTA
   const int n0 = blockIdx.x * BN;
 
   extern __shared__ uint8_t smem_raw[];
@@ -125,6 +124,16 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  // Everything above overlaps the previous kernel (PDL); from here on we read
+  // its outputs (A operand, row count, residual).
+  pdl_wait();
+  pdl_trigger();
+  const int M = ep.d_M ? *ep.d_M : ep.M;
+  if (m0 >= M) {  // uniform across the CTA
+    if (warp == 0) tmem_dealloc<kTmemCols>(tmem);
+    return;
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -197,6 +206,22 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     }
     const long long step_off =
         ep.d_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride : 0LL;
+    // BN = 32 (the N = d_model residual GEMMs): each epilogue warp owns one
+    // 32-row x 16-column chunk, so its residual and bias are fetched while
+    // the MMAs are still running.
+    constexpr bool kPrefetch = (BN == 32);
+    float res_pre[kPrefetch ? 32 : 1];
+    float bias_pre = 0.0f;
+    if constexpr (kPrefetch) {
+      const int col = n0 + half * kHalf + (lane % kChunk);
+      const bool col_ok = col < ep.N && lane < kChunk;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        res_pre[i] = (ep.residual && col_ok && i < nrows)
+                         ? ep.residual[static_cast<long long>(rbase + i) * ep.ldr + col]
+                         : 0.0f;
+      if (ep.bias && col_ok) bias_pre = ep.bias[col];
+    }
     mbar_wait(accum_bar, 0);
     tc_fence_after();
 #pragma unroll 1
@@ -228,6 +253,19 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       __syncwarp();
       const int col = n0 + c + (lane % kChunk);
       const bool col_ok = col < ep.N && lane < kChunk;
+      if constexpr (kPrefetch) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float v = stage[i * 33 + (lane % kChunk)];
+          if (ep.bias) v = __fadd_rn(v, bias_pre);
+          if (ep.relu) v = v > 0.0f ? v : 0.0f;
+          if (ep.residual) v = __fadd_rn(res_pre[i], v);
+          if (col_ok && i < nrows)
+            ep.C[step_off + static_cast<long long>(rbase + i) * ep.ldc + col] = v;
+        }
+        __syncwarp();
+        continue;
+      }
       const float bias = (col_ok && ep.bias) ? ep.bias[col] : 0.0f;
       // Residual loads of a row group are issued before its stores: C may
       // alias the residual, so loads placed after stores would serialise.

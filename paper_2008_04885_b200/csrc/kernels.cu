@@ -6,6 +6,7 @@
 
 #include "detmath.cuh"
 #include "errors.hpp"
+#include "launch.cuh"
 #include "kernels.cuh"
 
 namespace mtg {
@@ -55,6 +56,8 @@ __global__ void embed_src_kernel(const int* __restrict__ ids, const int* __restr
                                  const float* __restrict__ table, int d, float sqrt_d,
                                  const float* __restrict__ pe, float* __restrict__ out,
                                  long long ldo) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const float* e = table + static_cast<long long>(ids[r]) * d;
   const float* p = pe + static_cast<long long>(pos[r]) * d;
@@ -67,6 +70,8 @@ __global__ void embed_tgt_kernel(const int* __restrict__ prev, const int* d_rows
                                  const int8_t* __restrict__ table_q, float q_scale, int d,
                                  float sqrt_d, const float* __restrict__ pe,
                                  float* __restrict__ out, long long ldo) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
   const int t = *d_step;
@@ -90,6 +95,8 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
                                      const float* __restrict__ b, float* __restrict__ y,
                                      long long ldy, float* __restrict__ rowmax, OperandOut op,
                                      int has_op) {
+  pdl_wait();
+  pdl_trigger();
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -183,6 +190,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, long long ldx, int
                                  const float* __restrict__ b, float* __restrict__ y,
                                  long long ldy, float* __restrict__ rowmax, OperandOut op,
                                  int has_op) {
+  pdl_wait();
+  pdl_trigger();
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -221,6 +230,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, long long ldx, int
 
 __global__ void rowmax_kernel(const float* __restrict__ x, long long ldx, int rows, int n,
                               float* __restrict__ rowmax, int* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -241,6 +252,8 @@ __global__ void quantize_seg_kernel(const float* __restrict__ x, long long ldx, 
                                     const int* __restrict__ row_seg,
                                     const int* __restrict__ seg_off,
                                     const float* __restrict__ rowmax, OperandOut op) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -255,7 +268,7 @@ __global__ void quantize_seg_kernel(const float* __restrict__ x, long long ldx, 
 
 // One query against n keys, one warp. q: dh floats in smem; s: n floats of
 // per-warp smem scratch. P3 dots, P1 sum, context summed in key order.
-template <class KP, class VP>
+template <bool kVecKeys = true, class KP, class VP>
 __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float scale, KP kp,
                                             VP vp, float* s, float* out) {
   const int lane = threadIdx.x & 31;
@@ -263,7 +276,7 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
   for (int j = lane; j < n; j += 32) {
     const float* k = kp(j);
     float acc = 0.0f;
-    if ((dh & 3) == 0) {
+    if (kVecKeys && (dh & 3) == 0) {
       for (int c = 0; c < dh; c += 4) {
         const float4 kv = *reinterpret_cast<const float4*>(k + c);
         acc = __fadd_rn(acc, __fmul_rn(q[c], kv.x));
@@ -293,12 +306,12 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
     if (c < dh) {
       float acc = 0.0f;
       int j = 0;
-      for (; j + 4 <= n; j += 4) {
-        const float v0 = vp(j)[c], v1 = vp(j + 1)[c], v2 = vp(j + 2)[c], v3 = vp(j + 3)[c];
-        acc = __fadd_rn(acc, __fmul_rn(s[j], v0));
-        acc = __fadd_rn(acc, __fmul_rn(s[j + 1], v1));
-        acc = __fadd_rn(acc, __fmul_rn(s[j + 2], v2));
-        acc = __fadd_rn(acc, __fmul_rn(s[j + 3], v3));
+      for (; j + 8 <= n; j += 8) {  // 8 independent loads in flight per lane
+        float vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) vv[u] = vp(j + u)[c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, __fmul_rn(s[j + u], vv[u]));
       }
       for (; j < n; ++j) acc = __fadd_rn(acc, __fmul_rn(s[j], vp(j)[c]));
       out[c] = acc;
@@ -310,19 +323,31 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
 __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ldq,
                                      const int* __restrict__ off, int d, int dh, int max_len,
                                      float scale, float* __restrict__ ctx, long long ldc) {
+  pdl_wait();
+  pdl_trigger();
+  // K and V of this (sentence, head) are staged once in smem with coalesced
+  // loads; K rows are padded to dh+1 floats (lane j reads key row j).
   extern __shared__ float sm[];
   const int s = blockIdx.x, h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int r0 = off[s], n = off[s + 1] - r0;
-  float* qs = sm + warp * (dh + max_len);
+  float* Ks = sm;
+  float* Vs = Ks + max_len * (dh + 1);
+  float* qs = Vs + max_len * dh + warp * (dh + max_len);
   float* ss = qs + dh;
   const float* base = qkv + static_cast<long long>(r0) * ldq + h * dh;
+  for (int idx = threadIdx.x; idx < n * dh; idx += blockDim.x) {
+    const int j = idx / dh, c = idx - j * dh;
+    Ks[j * (dh + 1) + c] = base[j * ldq + d + c];
+    Vs[j * dh + c] = base[j * ldq + 2 * d + c];
+  }
+  __syncthreads();
   for (int i = warp; i < n; i += nw) {
     for (int c = lane; c < dh; c += 32) qs[c] = base[i * ldq + c];
     __syncwarp();
-    attend_warp(
-        qs, n, dh, scale, [&](int j) { return base + j * ldq + d; },
-        [&](int j) { return base + j * ldq + 2 * d; }, ss,
+    attend_warp<false>(
+        qs, n, dh, scale, [&](int j) { return Ks + j * (dh + 1); },
+        [&](int j) { return Vs + j * dh; }, ss,
         ctx + static_cast<long long>(r0 + i) * ldc + h * dh);
   }
 }
@@ -359,6 +384,8 @@ __global__ void dec_self_attention_kernel(const float* __restrict__ cache, int r
                                           const int* __restrict__ anc1, const int* d_rows,
                                           const int* d_step, int d, int dh, float scale,
                                           float* __restrict__ ctx, long long ldc, OperandOut op) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
@@ -393,6 +420,8 @@ __global__ void dec_cross_attention_kernel(const float* __restrict__ cq, long lo
                                            const int* __restrict__ enc_len, const int* d_rows,
                                            int max_src, int d, int dh, float scale,
                                            float* __restrict__ ctx, long long ldc, OperandOut op) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
@@ -468,6 +497,8 @@ constexpr int kTopkListCap = 1024;
 template <int NV4>
 __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restrict__ logits,
                                                             long long ldl, BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;
   __shared__ float red_f[32];
@@ -619,7 +650,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
 void launch_embed_src(const int* ids, const int* pos, int rows, const float* table, int d,
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st) {
   if (rows <= 0) return;
-  embed_src_kernel<<<rows, 128, 0, st>>>(ids, pos, table, d, sqrt_d, pe, out, ldo);
+  launch_k(embed_src_kernel, rows, 128, 0, st, ids, pos, table, d, sqrt_d, pe, out, ldo);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -627,7 +658,7 @@ void launch_embed_tgt(const int* prev, const int* d_rows, int max_rows, const in
                       const float* table, const int8_t* table_q, float q_scale, int d,
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st) {
   if (max_rows <= 0) return;
-  embed_tgt_kernel<<<max_rows, 128, 0, st>>>(prev, d_rows, d_step, table, table_q, q_scale, d,
+  launch_k(embed_tgt_kernel, max_rows, 128, 0, st, prev, d_rows, d_step, table, table_q, q_scale, d,
                                              sqrt_d, pe, out, ldo);
   MTG_CUDA(cudaGetLastError());
 }
@@ -642,16 +673,16 @@ void launch_layernorm(const float* x, long long ldx, int max_rows, const int* d_
   const int has = op ? 1 : 0;
   const int kpl = (n + 31) / 32;
   if (kpl <= 1)
-    layernorm_reg_kernel<1><<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy,
+    launch_k(layernorm_reg_kernel<1>, grid, block, 0, st, x, ldx, max_rows, d_rows, n, g, b, y, ldy,
                                                      rowmax, o, has);
   else if (kpl <= 4)
-    layernorm_reg_kernel<4><<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy,
+    launch_k(layernorm_reg_kernel<4>, grid, block, 0, st, x, ldx, max_rows, d_rows, n, g, b, y, ldy,
                                                      rowmax, o, has);
   else if (kpl <= 16)
-    layernorm_reg_kernel<16><<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy,
+    launch_k(layernorm_reg_kernel<16>, grid, block, 0, st, x, ldx, max_rows, d_rows, n, g, b, y, ldy,
                                                       rowmax, o, has);
   else
-    layernorm_kernel<<<grid, block, 0, st>>>(x, ldx, max_rows, d_rows, n, g, b, y, ldy, rowmax, o,
+    launch_k(layernorm_kernel, grid, block, 0, st, x, ldx, max_rows, d_rows, n, g, b, y, ldy, rowmax, o,
                                              has);
   MTG_CUDA(cudaGetLastError());
 }
@@ -660,7 +691,7 @@ void launch_rowmax(const float* x, long long ldx, int rows, int n, float* rowmax
                    cudaStream_t st) {
   if (rows <= 0) return;
   const int wpb = 8;
-  rowmax_kernel<<<(rows + wpb - 1) / wpb, wpb * 32, 0, st>>>(x, ldx, rows, n, rowmax, nonfinite);
+  launch_k(rowmax_kernel, (rows + wpb - 1) / wpb, wpb * 32, 0, st, x, ldx, rows, n, rowmax, nonfinite);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -669,7 +700,7 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
                          cudaStream_t st) {
   if (rows <= 0) return;
   const int wpb = 8;
-  quantize_seg_kernel<<<(rows + wpb - 1) / wpb, wpb * 32, 0, st>>>(x, ldx, rows, n, row_seg,
+  launch_k(quantize_seg_kernel, (rows + wpb - 1) / wpb, wpb * 32, 0, st, x, ldx, rows, n, row_seg,
                                                                    seg_off, rowmax, op);
   MTG_CUDA(cudaGetLastError());
 }
@@ -679,9 +710,19 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
                           cudaStream_t st) {
   if (n_sent <= 0) return;
   const int dh = d / heads;
-  const int nw = 4;
-  const size_t smem = sizeof(float) * nw * (dh + max_len);
-  enc_attention_kernel<<<dim3(n_sent, heads), nw * 32, smem, st>>>(qkv, ldq, off, d, dh, max_len,
+  const int nw = 8;
+  const size_t smem =
+      sizeof(float) * (size_t(max_len) * (2 * dh + 1) + size_t(nw) * (dh + max_len));
+  static size_t configured = 48 * 1024;
+  if (smem > 227 * 1024)
+    fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
+  if (smem > configured) {
+    MTG_CUDA(cudaFuncSetAttribute(enc_attention_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = smem;
+  }
+  launch_k(enc_attention_kernel, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len,
                                                                    scale, ctx, ldc);
   MTG_CUDA(cudaGetLastError());
 }
@@ -693,7 +734,7 @@ void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const i
   if (r_max <= 0) return;
   const int dh = d / heads;
   const size_t smem = sizeof(float) * (d + 33 + T + heads * (dh + T));
-  dec_self_attention_kernel<<<r_max, heads * 32, smem, st>>>(qkv_cache, r_max, T, anc0, anc1,
+  launch_k(dec_self_attention_kernel, r_max, heads * 32, smem, st, qkv_cache, r_max, T, anc0, anc1,
                                                              d_rows, d_step, d, dh, scale, ctx,
                                                              ldc, op);
   MTG_CUDA(cudaGetLastError());
@@ -707,7 +748,7 @@ void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv
   if (max_rows <= 0) return;
   const int dh = d / heads;
   const size_t smem = sizeof(float) * (d + 33 + heads * (dh + max_src));
-  dec_cross_attention_kernel<<<max_rows, heads * 32, smem, st>>>(
+  launch_k(dec_cross_attention_kernel, max_rows, heads * 32, smem, st, 
       cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows, max_src, d, dh, scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
 }
@@ -715,7 +756,7 @@ void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv
 template <int NV4>
 static void launch_topk_nv(const float* logits, long long ldl, const BeamDev& b,
                            cudaStream_t st) {
-  topk_kernel<NV4><<<b.R_max, kTopkThreads, 0, st>>>(logits, ldl, b);
+  launch_k(topk_kernel<NV4>, b.R_max, kTopkThreads, 0, st, logits, ldl, b);
 }
 
 void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st) {

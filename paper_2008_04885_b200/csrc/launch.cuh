@@ -1,0 +1,47 @@
+// Kernel launch helper: every kernel of the path is launched with
+// programmatic dependent launch (PDL) enabled, so a kernel's CTAs can start
+// (TMEM allocation, barrier init, tensor-map prefetch) while its predecessor
+// drains. Kernels call pdl_wait() before touching predecessor outputs and
+// pdl_trigger() right after, which keeps the usual stream ordering for data.
+// MTG_NO_PDL=1 in the environment launches plainly (debugging).
+#pragma once
+
+#include <cstdlib>
+#include <utility>
+
+#include <cuda_runtime.h>
+
+#include "errors.hpp"
+
+namespace mtg {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MTG_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  MTG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+}  // namespace mtg

@@ -1,6 +1,7 @@
 #include "prep.cuh"
 
 #include "errors.hpp"
+#include "launch.cuh"
 
 namespace mtg {
 
@@ -30,6 +31,8 @@ __global__ void quantize_segments_kernel(const float* __restrict__ x, long long 
                                          int n_seg, const int* d_n_seg,
                                          int8_t* __restrict__ q, int k_pad,
                                          float* __restrict__ row_scale, int* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.x;
   const int ns = d_n_seg ? *d_n_seg : n_seg;
   if (s >= ns) return;
@@ -69,6 +72,8 @@ __global__ void quantize_rows_kernel(const float* __restrict__ x, long long ld_x
                                      int max_rows, const int* d_rows,
                                      int8_t* __restrict__ q, int k_pad,
                                      float* __restrict__ row_scale, int* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -95,6 +100,8 @@ __global__ void quantize_rows_reg_kernel(const float* __restrict__ x, long long 
                                          int max_rows, const int* d_rows,
                                          int8_t* __restrict__ q, int k_pad,
                                          float* __restrict__ row_scale, int* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -126,6 +133,8 @@ __global__ void quantize_rows_reg_kernel(const float* __restrict__ x, long long 
 __global__ void cast_bf16_kernel(const float* __restrict__ x, long long ld_x, int k,
                                  int max_rows, const int* d_rows,
                                  __nv_bfloat16* __restrict__ out, int k_pad) {
+  pdl_wait();
+  pdl_trigger();
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.y;
   if (r >= rows) return;
@@ -137,6 +146,8 @@ __global__ void cast_bf16_kernel(const float* __restrict__ x, long long ld_x, in
 __global__ void split_tf32_kernel(const float* __restrict__ x, long long ld_x, int k,
                                   int max_rows, const int* d_rows, float* __restrict__ hi,
                                   float* __restrict__ lo, int k_pad) {
+  pdl_wait();
+  pdl_trigger();
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.y;
   if (r >= rows) return;
@@ -157,7 +168,7 @@ void launch_quantize_segments(const float* x, long long ld_x, int k, const int* 
                               int n_seg, const int* d_n_seg, int8_t* q, int k_pad,
                               float* row_scale, int* nonfinite_flag, cudaStream_t st) {
   if (n_seg <= 0) return;
-  quantize_segments_kernel<<<n_seg, 256, 0, st>>>(x, ld_x, k, seg_off, n_seg, d_n_seg, q,
+  launch_k(quantize_segments_kernel, n_seg, 256, 0, st, x, ld_x, k, seg_off, n_seg, d_n_seg, q,
                                                   k_pad, row_scale, nonfinite_flag);
   MTG_CUDA(cudaGetLastError());
 }
@@ -170,13 +181,13 @@ void launch_quantize_rows(const float* x, long long ld_x, int k, int max_rows,
   const dim3 grid((max_rows + wpb - 1) / wpb), block(wpb * 32);
   const int kpl = (k + 31) / 32;
   if (kpl <= 16)
-    quantize_rows_reg_kernel<16><<<grid, block, 0, st>>>(x, ld_x, k, max_rows, d_rows, q, k_pad,
+    launch_k(quantize_rows_reg_kernel<16>, grid, block, 0, st, x, ld_x, k, max_rows, d_rows, q, k_pad,
                                                          row_scale, nonfinite_flag);
   else if (kpl <= 64)
-    quantize_rows_reg_kernel<64><<<grid, block, 0, st>>>(x, ld_x, k, max_rows, d_rows, q, k_pad,
+    launch_k(quantize_rows_reg_kernel<64>, grid, block, 0, st, x, ld_x, k, max_rows, d_rows, q, k_pad,
                                                          row_scale, nonfinite_flag);
   else
-    quantize_rows_kernel<<<grid, block, 0, st>>>(x, ld_x, k, max_rows, d_rows, q, k_pad,
+    launch_k(quantize_rows_kernel, grid, block, 0, st, x, ld_x, k, max_rows, d_rows, q, k_pad,
                                                  row_scale, nonfinite_flag);
   MTG_CUDA(cudaGetLastError());
 }
@@ -185,7 +196,7 @@ void launch_cast_bf16(const float* x, long long ld_x, int k, int max_rows,
                       const int* d_rows, __nv_bfloat16* out, int k_pad, cudaStream_t st) {
   if (max_rows <= 0) return;
   dim3 grid((k_pad + 255) / 256, max_rows);
-  cast_bf16_kernel<<<grid, 256, 0, st>>>(x, ld_x, k, max_rows, d_rows, out, k_pad);
+  launch_k(cast_bf16_kernel, grid, 256, 0, st, x, ld_x, k, max_rows, d_rows, out, k_pad);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -194,7 +205,7 @@ void launch_split_tf32(const float* x, long long ld_x, int k, int max_rows,
                        cudaStream_t st) {
   if (max_rows <= 0) return;
   dim3 grid((k_pad + 255) / 256, max_rows);
-  split_tf32_kernel<<<grid, 256, 0, st>>>(x, ld_x, k, max_rows, d_rows, hi, lo, k_pad);
+  launch_k(split_tf32_kernel, grid, 256, 0, st, x, ld_x, k, max_rows, d_rows, hi, lo, k_pad);
   MTG_CUDA(cudaGetLastError());
 }
 
