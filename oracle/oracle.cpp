@@ -9,6 +9,7 @@
 //                     P1 butterfly across the 16 warp sums (+16 zero lanes).
 //                     (block_sum_512)
 //   P3 dot          : acc = 0; acc = acc + a[c]*b[c] for c ascending (no FMA).
+//   attention ctx   : ctx[c] = P1 sum over keys j of p_j * v_j[c].
 //   P4 exp/log/pow  : detmath.h.
 //   P5 f32 GEMM     : per output element, k-ascending mul+add (gemm_rows order,
 //                     tensor.cpp:113-123); the GPU uses 3xTF32 tensor cores,
@@ -725,10 +726,13 @@ void attend_row(const float* q, const float* K, Index ldk, const float* V, Index
   for (Index j = 0; j < n; ++j) s[j] = orc_expf(s[j] - mx);
   const float sum = warp_sum(s.data(), n);
   for (Index j = 0; j < n; ++j) s[j] = s[j] / sum;
+  // ctx[c] = P1 sum over keys of p_j * v_j[c] (the GPU's lanes own keys and
+  // reduce-scatter the per-column partials; same tree as P1).
+  static thread_local std::vector<float> prod;
+  prod.resize(static_cast<size_t>(n));
   for (Index c = 0; c < dh; ++c) {
-    float acc = 0.0f;
-    for (Index j = 0; j < n; ++j) acc = acc + s[j] * V[j * ldv + c];
-    ctx[c] = acc;
+    for (Index j = 0; j < n; ++j) prod[j] = s[j] * V[j * ldv + c];
+    ctx[c] = warp_sum(prod.data(), n);
   }
 }
 

@@ -266,8 +266,26 @@ __global__ void quantize_seg_kernel(const float* __restrict__ x, long long ldx, 
 
 // ---- attention ---------------------------------------------------------------------------
 
+// Sums 32 per-lane partial vectors: lane l returns sum over lanes of a[l].
+// Pairs lanes differing in bit 4, then 3, ..., 0 -- the same tree as the
+// xor-butterfly P1 sum, so each column is bit-identical to warp_allsum.
+__device__ __forceinline__ float reduce_scatter32(float (&a)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = upper ? a[i] : a[i + w];
+      const float keep = upper ? a[i + w] : a[i];
+      a[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, w));
+    }
+  }
+  return a[0];
+}
+
 // One query against n keys, one warp. q: dh floats in smem; s: n floats of
-// per-warp smem scratch. P3 dots, P1 sum, context summed in key order.
+// per-warp smem scratch. P3 dots, P1 sums (softmax denominator and context).
 template <bool kVecKeys = true, class KP, class VP>
 __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float scale, KP kp,
                                             VP vp, float* s, float* out) {
@@ -301,21 +319,36 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
   const float sum = warp_allsum(part);
   for (int j = lane; j < n; j += 32) s[j] = __fdiv_rn(s[j], sum);
   __syncwarp();
+  // Context: lanes own keys j = lane + 32u and accumulate p_j * v_j[c] for a
+  // 32-column chunk, then a reduce-scatter butterfly leaves column c0+lane in
+  // lane `lane` (per column the same tree as the P1 warp sum).
   for (int c0 = 0; c0 < dh; c0 += 32) {
-    const int c = c0 + lane;
-    if (c < dh) {
-      float acc = 0.0f;
-      int j = 0;
-      for (; j + 8 <= n; j += 8) {  // 8 independent loads in flight per lane
-        float vv[8];
+    float acc[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) vv[u] = vp(j + u)[c];
+    for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+    const bool full = kVecKeys && c0 + 32 <= dh && (dh & 3) == 0;
+    for (int j = lane; j < n; j += 32) {
+      const float p = s[j];
+      const float* v = vp(j) + c0;
+      float vv[32];
+      if (full) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, __fmul_rn(s[j + u], vv[u]));
+        for (int i = 0; i < 32; i += 4) {
+          const float4 f = *reinterpret_cast<const float4*>(v + i);
+          vv[i] = f.x;
+          vv[i + 1] = f.y;
+          vv[i + 2] = f.z;
+          vv[i + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) vv[i] = c0 + i < dh ? v[i] : 0.0f;
       }
-      for (; j < n; ++j) acc = __fadd_rn(acc, __fmul_rn(s[j], vp(j)[c]));
-      out[c] = acc;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(p, vv[i]));
     }
+    const float col = reduce_scatter32(acc);
+    if (c0 + lane < dh) out[c0 + lane] = col;
   }
   __syncwarp();
 }
@@ -450,6 +483,19 @@ __device__ __forceinline__ bool better2(float a, int ta, float b, int tb) {
 
 // One 512-thread CTA per live row; thread t owns logits 4(t + 512 i) + c,
 // i < NV4, held in registers (one HBM pass). P2 sum order.
+// Warp-wide argmax of (score desc, token asc); every lane gets the winner.
+__device__ __forceinline__ void warp_best(float& bs, int& bt) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+    const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ot != INT_MAX && (bt == INT_MAX || better2(os, ot, bs, bt))) {
+      bs = os;
+      bt = ot;
+    }
+  }
+}
+
 // Block-wide argmax of (score desc, token asc) over one candidate per
 // thread; returns the winner in every thread. red_f/red_i: >= 32 entries.
 __device__ __forceinline__ void block_best(float& bs, int& bt, float* red_f, int* red_i) {
@@ -552,22 +598,59 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
   const int kB = min(b.B, V);
 
   // tau: kB-th largest per-thread max (thread index breaks value ties).
-  // Fewer than kB threads holding logits: no bound, keep everything.
-  float tau = kNegInf;
+  // tau = kB-th largest per-thread max: each warp finds its top-kB thread
+  // maxima with shuffles, warp 0 picks the kB-th of the union. Fewer than kB
+  // threads holding logits: no bound (tau = -inf), keep everything.
+  __shared__ float wl_s[kWarps * kMaxBeam];
+  __shared__ int wl_t[kWarps * kMaxBeam];
+  __shared__ float tau_sh;
   {
     float mine = tmax;
     for (int k = 0; k < kB; ++k) {
       float bs = mine;
       int bt = mine == kNegInf ? INT_MAX : tid;
-      block_best(bs, bt, red_f, red_i);  // larger value first, lower tid on ties
-      if (bt == INT_MAX) {
-        tau = kNegInf;
-        break;
+      warp_best(bs, bt);
+      if (lane == 0) {
+        wl_s[warp * kMaxBeam + k] = bs;
+        wl_t[warp * kMaxBeam + k] = bt;
       }
-      tau = bs;
       if (bt == tid) mine = kNegInf;
     }
   }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int kPer = kWarps * kMaxBeam / 32;  // entries per lane
+    unsigned taken = 0u;
+    float tau = kNegInf;
+    for (int k = 0; k < kB; ++k) {
+      float bs = kNegInf;
+      int bt = INT_MAX, be = -1;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        const int idx = lane + 32 * e;
+        const int w = idx / kMaxBeam, kk = idx % kMaxBeam;
+        if (kk < kB && !((taken >> e) & 1u) && wl_t[idx] != INT_MAX &&
+            (bt == INT_MAX || better2(wl_s[idx], wl_t[idx], bs, bt))) {
+          bs = wl_s[idx];
+          bt = wl_t[idx];
+          be = e;
+        }
+        (void)w;
+      }
+      float ws = bs;
+      int wt = bt;
+      warp_best(ws, wt);
+      if (wt == INT_MAX) {
+        tau = kNegInf;
+        break;
+      }
+      tau = ws;
+      if (bt == wt && be >= 0) taken |= 1u << be;
+    }
+    if (lane == 0) tau_sh = tau;
+  }
+  __syncthreads();
+  const float tau = tau_sh;
   const float s_lb = tau == kNegInf ? kNegInf : __fadd_rn(plp, __fsub_rn(tau, lse));
 #pragma unroll
   for (int i = 0; i < NV4; ++i)
@@ -587,6 +670,34 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restr
     }
   __syncthreads();
   const int n_list = list_n;
+
+  if (n_list <= 64) {  // common case: warp 0 alone, shuffles only
+    if (warp != 0) return;
+    unsigned taken = 0u;
+    for (int k = 0; k < kB; ++k) {
+      float bs = kNegInf;
+      int bt = INT_MAX, be = -1;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int idx = lane + 32 * e;
+        if (idx < n_list && !((taken >> e) & 1u) &&
+            (bt == INT_MAX || better2(list_s[idx], list_t[idx], bs, bt))) {
+          bs = list_s[idx];
+          bt = list_t[idx];
+          be = e;
+        }
+      }
+      float ws = bs;
+      int wt = bt;
+      warp_best(ws, wt);
+      if (lane == 0) {
+        b.cand_score[static_cast<long long>(r) * b.B + k] = ws;
+        b.cand_tok[static_cast<long long>(r) * b.B + k] = wt;
+      }
+      if (bt == wt && be >= 0) taken |= 1u << be;
+    }
+    return;
+  }
 
   if (n_list <= kTopkListCap) {
     unsigned taken = 0u;  // entries tid + 512 e, e < 2
