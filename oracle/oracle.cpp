@@ -4,10 +4,9 @@
 // this file agree on the ones below):
 //   P1 lane sum     : 32 partials, partial l = sum of v[l], v[l+32], ... in
 //                     order, then xor-butterfly (16,8,4,2,1). (warp_sum)
-//   P2 block sum    : 512 partials, partial t = sum over i of v[4(t+512i)+c],
+//   P2 block sum    : 1024 partials, partial t = sum over i of v[4(t+1024i)+c],
 //                     c = 0..3, in order; P1 butterfly per 32-thread warp, then
-//                     P1 butterfly across the 16 warp sums (+16 zero lanes).
-//                     (block_sum_512)
+//                     P1 butterfly across the 32 warp sums. (block_sum_1024)
 //   P3 dot          : acc = 0; acc = acc + a[c]*b[c] for c ascending (no FMA).
 //   attention ctx   : ctx[c] = P1 sum over keys j of p_j * v_j[c].
 //   P4 exp/log/pow  : detmath.h.
@@ -686,10 +685,9 @@ float butterfly32(float* p) {
   return p[0];
 }
 
-// P2 (512 threads = 16 warps; the 16 warp sums are butterflied in one warp
-// with lanes 16..31 contributing 0).
-float block_sum_512(const float* v, Index n) {
-  constexpr int kT = 512;
+// P2 (1024 threads = 32 warps; the 32 warp sums are butterflied in one warp).
+float block_sum_1024(const float* v, Index n) {
+  constexpr int kT = 1024;
   static thread_local std::vector<float> part(kT);
   for (int t = 0; t < kT; ++t) {
     float s = 0.0f;
@@ -1107,7 +1105,7 @@ std::vector<float> log_softmax_row(const float* x, int n) {
   for (int j = 0; j < n; ++j) mx = std::max(mx, x[j]);
   std::vector<float> e(static_cast<size_t>(n));
   for (int j = 0; j < n; ++j) e[j] = orc_expf(x[j] - mx);
-  const float lse = orc_logf(block_sum_512(e.data(), n)) + mx;
+  const float lse = orc_logf(block_sum_1024(e.data(), n)) + mx;
   for (int j = 0; j < n; ++j) e[j] = x[j] - lse;
   return e;
 }

@@ -232,7 +232,7 @@ struct BeamConfig {
   float length_penalty_alpha = 1.0f;
 };
 
-// log-softmax of one logits row in the GPU's 512-thread reduction order.
+// log-softmax of one logits row in the GPU's 1024-thread reduction order.
 std::vector<float> log_softmax_row(const float* x, int n);
 
 Hypothesis beam_search(const Executor& ex, const std::vector<int>& src_ids,

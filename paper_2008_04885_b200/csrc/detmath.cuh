@@ -36,10 +36,11 @@ __device__ __forceinline__ float det_expf(float x) {
   return p;
 }
 
-// det_expf for finite x <= 0 (softmax arguments x - max): same bits, minus
-// the NaN / overflow branches.
+// det_expf for x <= 0 (softmax arguments x - max, -inf allowed): same bits,
+// branch-free (both scalings computed, then selected).
 __device__ __forceinline__ float det_expf_nonpos(float x) {
-  if (x < -103.97208404541015625f) return 0.0f;
+  const bool under = x < -103.97208404541015625f;
+  x = under ? 0.0f : x;
   const float n = rintf(__fmul_rn(x, 1.44269502162933349609375f));
   float r = __fmaf_rn(n, -0.693359375f, x);
   r = __fmaf_rn(n, 2.12194440e-4f, r);
@@ -53,11 +54,13 @@ __device__ __forceinline__ float det_expf_nonpos(float x) {
   p = __fmaf_rn(p, z, r);
   p = __fadd_rn(p, 1.0f);
   const int ni = static_cast<int>(n);
+  // Normal result: scaling by 2^n is exact, so adding n to the exponent
+  // gives the same bits as the two multiplies.
+  const float fast = __int_as_float(__float_as_int(p) + (ni << 23));
   const int n1 = ni / 2;
-  const int n2 = ni - n1;
-  p = __fmul_rn(p, __int_as_float((n1 + 127) << 23));
-  p = __fmul_rn(p, __int_as_float((n2 + 127) << 23));
-  return p;
+  const float slow = __fmul_rn(__fmul_rn(p, __int_as_float((n1 + 127) << 23)),
+                               __int_as_float((ni - n1 + 127) << 23));
+  return under ? 0.0f : (ni >= -125 ? fast : slow);
 }
 
 __device__ __forceinline__ float det_logf(float x) {

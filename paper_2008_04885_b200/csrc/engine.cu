@@ -19,7 +19,6 @@ int gemm_prec_of(int prec) {
   return prec == kINT8 ? kPrecI8 : prec == kBF16 ? kPrecBF16 : kPrecTF32x3;
 }
 
-int round4(int v) { return (v + 3) / 4 * 4; }
 
 // Converts fp32 K-major rows (host, [n x k]) into the operand format.
 void upload_f32_operand(const std::vector<float>& kmaj, int n, int k, int prec, DevLinear& L,
@@ -168,7 +167,7 @@ Engine::Engine(HostModel model, int precision, int device)
   d_ = c.d_model;
   dff_ = c.d_ff;
   V_ = c.tgt_vocab_size;
-  Vp_ = round4(V_);
+  Vp_ = static_cast<int>(topk_pitch(V_));  // pad columns hold -inf (top-k)
   T_ = c.max_seq_len;
   heads_ = c.num_heads;
   upload_weights();
@@ -277,6 +276,11 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   dec_ctx_.resize(r_max_ * d);
   dec_cq_.resize(r_max_ * d);
   logits_.resize(size_t(r_max_) * Vp_);
+  // The GEMM writes columns < V only; the pad stays -inf (adds exp(-inf) = 0
+  // to the log-softmax sum and never scores).
+  launch_fill(logits_.get(), static_cast<long long>(r_max_) * Vp_, -__builtin_huge_valf(),
+              stream_);
+  MTG_CUDA(cudaStreamSynchronize(stream_));
   qkv_cache_.clear();
   qkv_cache_.resize(c.num_decoder_layers);
   for (auto& b : qkv_cache_) b.resize(size_t(T_) * r_max_ * 3 * d);

@@ -412,7 +412,8 @@ __device__ __forceinline__ void finish_ctx_row(const float* row, int d, long lon
   write_operand(op, r, row, d, qscale_of(red[32]), tid, blockDim.x);
 }
 
-__global__ void dec_self_attention_kernel(const float* __restrict__ cache, int r_max, int T,
+__global__ void __launch_bounds__(256, 3)
+    dec_self_attention_kernel(const float* __restrict__ cache, int r_max, int T,
                                           const int* __restrict__ anc0,
                                           const int* __restrict__ anc1, const int* d_rows,
                                           const int* d_step, int d, int dh, float scale,
@@ -446,7 +447,8 @@ __global__ void dec_self_attention_kernel(const float* __restrict__ cache, int r
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
 
-__global__ void dec_cross_attention_kernel(const float* __restrict__ cq, long long ldq,
+__global__ void __launch_bounds__(256, 3)
+    dec_cross_attention_kernel(const float* __restrict__ cq, long long ldq,
                                            const float* __restrict__ ckv,
                                            const int* __restrict__ row_sent,
                                            const int* __restrict__ enc_off,
@@ -473,285 +475,6 @@ __global__ void dec_cross_attention_kernel(const float* __restrict__ cq, long lo
       [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; }, ss, row + h * dh);
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
-}
-
-// ---- log-softmax + top-k -----------------------------------------------------------------
-
-__device__ __forceinline__ bool better2(float a, int ta, float b, int tb) {
-  return a > b || (a == b && ta < tb);
-}
-
-// One 512-thread CTA per live row; thread t owns logits 4(t + 512 i) + c,
-// i < NV4, held in registers (one HBM pass). P2 sum order.
-// Warp-wide argmax of (score desc, token asc); every lane gets the winner.
-__device__ __forceinline__ void warp_best(float& bs, int& bt) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-    const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-    if (ot != INT_MAX && (bt == INT_MAX || better2(os, ot, bs, bt))) {
-      bs = os;
-      bt = ot;
-    }
-  }
-}
-
-// Block-wide argmax of (score desc, token asc) over one candidate per
-// thread; returns the winner in every thread. red_f/red_i: >= 32 entries.
-__device__ __forceinline__ void block_best(float& bs, int& bt, float* red_f, int* red_i) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kWarps = kTopkThreads / 32;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-    const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-    if (ot != INT_MAX && (bt == INT_MAX || better2(os, ot, bs, bt))) {
-      bs = os;
-      bt = ot;
-    }
-  }
-  __syncthreads();
-  if (lane == 0) {
-    red_f[warp] = bs;
-    red_i[warp] = bt;
-  }
-  __syncthreads();
-  bs = lane < kWarps ? red_f[lane] : kNegInf;
-  bt = lane < kWarps ? red_i[lane] : INT_MAX;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-    const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-    if (ot != INT_MAX && (bt == INT_MAX || better2(os, ot, bs, bt))) {
-      bs = os;
-      bt = ot;
-    }
-  }
-}
-
-constexpr int kTopkListCap = 1024;
-
-// One 512-thread CTA per live row; thread t owns logits 4(t + 512 i) + c,
-// i < NV4, held in registers (one HBM pass). P2 sum order.
-//
-// Top-kB by (score desc, token asc), score = fl(parent + fl(x - lse)), exact:
-// tau = kB-th largest per-thread max is <= the kB-th largest logit, and score
-// is monotone in x, so every true top-kB element has score >= score(tau).
-// Those elements go to a shared list (normally ~kB entries) and are selected
-// exactly; rows whose list overflows (e.g. all-equal logits) take the exact
-// slow path over every element.
-template <int NV4>
-__global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restrict__ logits,
-                                                            long long ldl, BeamDev b) {
-  pdl_wait();
-  pdl_trigger();
-  const int r = blockIdx.x;
-  if (r >= *b.n_rows) return;
-  __shared__ float red_f[32];
-  __shared__ int red_i[32];
-  __shared__ float list_s[kTopkListCap];
-  __shared__ int list_t[kTopkListCap];
-  __shared__ int list_n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kTopkThreads / 32;
-  const int V = b.V;
-  const float* x = logits + r * ldl;
-  if (tid == 0) list_n = 0;
-
-  float v[NV4 * 4];
-#pragma unroll
-  for (int i = 0; i < NV4; ++i) {
-    const int base = 4 * (tid + kTopkThreads * i);
-    if (base + 3 < V) {
-      const float4 f = *reinterpret_cast<const float4*>(x + base);
-      v[4 * i] = f.x;
-      v[4 * i + 1] = f.y;
-      v[4 * i + 2] = f.z;
-      v[4 * i + 3] = f.w;
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[4 * i + c] = base + c < V ? x[base + c] : kNegInf;
-    }
-  }
-  float tmax = kNegInf;
-#pragma unroll
-  for (int i = 0; i < NV4 * 4; ++i) tmax = fmaxf(tmax, v[i]);
-  float mx = warp_allmax(tmax);
-  if (lane == 0) red_f[warp] = mx;
-  __syncthreads();
-  mx = warp_allmax(lane < kWarps ? red_f[lane] : kNegInf);
-  __syncthreads();
-
-  float part = 0.0f;
-#pragma unroll
-  for (int i = 0; i < NV4; ++i)
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (4 * (tid + kTopkThreads * i) + c < V)
-        part = __fadd_rn(part, det_expf_nonpos(__fsub_rn(v[4 * i + c], mx)));
-  part = warp_allsum(part);
-  if (lane == 0) red_f[warp] = part;
-  __syncthreads();
-  const float total = warp_allsum(lane < kWarps ? red_f[lane] : 0.0f);
-  const float lse = __fadd_rn(det_logf(total), mx);
-  const float plp = b.row_lp[r];
-  const int kB = min(b.B, V);
-
-  // tau: kB-th largest per-thread max (thread index breaks value ties).
-  // tau = kB-th largest per-thread max: each warp finds its top-kB thread
-  // maxima with shuffles, warp 0 picks the kB-th of the union. Fewer than kB
-  // threads holding logits: no bound (tau = -inf), keep everything.
-  __shared__ float wl_s[kWarps * kMaxBeam];
-  __shared__ int wl_t[kWarps * kMaxBeam];
-  __shared__ float tau_sh;
-  {
-    float mine = tmax;
-    for (int k = 0; k < kB; ++k) {
-      float bs = mine;
-      int bt = mine == kNegInf ? INT_MAX : tid;
-      warp_best(bs, bt);
-      if (lane == 0) {
-        wl_s[warp * kMaxBeam + k] = bs;
-        wl_t[warp * kMaxBeam + k] = bt;
-      }
-      if (bt == tid) mine = kNegInf;
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    constexpr int kPer = kWarps * kMaxBeam / 32;  // entries per lane
-    unsigned taken = 0u;
-    float tau = kNegInf;
-    for (int k = 0; k < kB; ++k) {
-      float bs = kNegInf;
-      int bt = INT_MAX, be = -1;
-#pragma unroll
-      for (int e = 0; e < kPer; ++e) {
-        const int idx = lane + 32 * e;
-        const int w = idx / kMaxBeam, kk = idx % kMaxBeam;
-        if (kk < kB && !((taken >> e) & 1u) && wl_t[idx] != INT_MAX &&
-            (bt == INT_MAX || better2(wl_s[idx], wl_t[idx], bs, bt))) {
-          bs = wl_s[idx];
-          bt = wl_t[idx];
-          be = e;
-        }
-        (void)w;
-      }
-      float ws = bs;
-      int wt = bt;
-      warp_best(ws, wt);
-      if (wt == INT_MAX) {
-        tau = kNegInf;
-        break;
-      }
-      tau = ws;
-      if (bt == wt && be >= 0) taken |= 1u << be;
-    }
-    if (lane == 0) tau_sh = tau;
-  }
-  __syncthreads();
-  const float tau = tau_sh;
-  const float s_lb = tau == kNegInf ? kNegInf : __fadd_rn(plp, __fsub_rn(tau, lse));
-#pragma unroll
-  for (int i = 0; i < NV4; ++i)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = 4 * (tid + kTopkThreads * i) + c;
-      if (j < V) {
-        const float sc = __fadd_rn(plp, __fsub_rn(v[4 * i + c], lse));
-        if (sc >= s_lb) {
-          const int slot = atomicAdd(&list_n, 1);
-          if (slot < kTopkListCap) {
-            list_s[slot] = sc;
-            list_t[slot] = j;
-          }
-        }
-      }
-    }
-  __syncthreads();
-  const int n_list = list_n;
-
-  if (n_list <= 64) {  // common case: warp 0 alone, shuffles only
-    if (warp != 0) return;
-    unsigned taken = 0u;
-    for (int k = 0; k < kB; ++k) {
-      float bs = kNegInf;
-      int bt = INT_MAX, be = -1;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int idx = lane + 32 * e;
-        if (idx < n_list && !((taken >> e) & 1u) &&
-            (bt == INT_MAX || better2(list_s[idx], list_t[idx], bs, bt))) {
-          bs = list_s[idx];
-          bt = list_t[idx];
-          be = e;
-        }
-      }
-      float ws = bs;
-      int wt = bt;
-      warp_best(ws, wt);
-      if (lane == 0) {
-        b.cand_score[static_cast<long long>(r) * b.B + k] = ws;
-        b.cand_tok[static_cast<long long>(r) * b.B + k] = wt;
-      }
-      if (bt == wt && be >= 0) taken |= 1u << be;
-    }
-    return;
-  }
-
-  if (n_list <= kTopkListCap) {
-    unsigned taken = 0u;  // entries tid + 512 e, e < 2
-    for (int k = 0; k < kB; ++k) {
-      float bs = kNegInf;
-      int bt = INT_MAX;
-#pragma unroll
-      for (int e = 0; e < kTopkListCap / kTopkThreads; ++e) {
-        const int idx = tid + kTopkThreads * e;
-        if (idx < n_list && !((taken >> e) & 1u) &&
-            (bt == INT_MAX || better2(list_s[idx], list_t[idx], bs, bt))) {
-          bs = list_s[idx];
-          bt = list_t[idx];
-        }
-      }
-      block_best(bs, bt, red_f, red_i);
-      if (tid == 0) {
-        b.cand_score[static_cast<long long>(r) * b.B + k] = bs;
-        b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
-      }
-#pragma unroll
-      for (int e = 0; e < kTopkListCap / kTopkThreads; ++e) {
-        const int idx = tid + kTopkThreads * e;
-        if (idx < n_list && list_t[idx] == bt) taken |= 1u << e;
-      }
-    }
-    return;
-  }
-
-  // Slow exact path: kB rounds over every element with a taken mask.
-  unsigned long long taken = 0ull;
-  for (int k = 0; k < kB; ++k) {
-    float bs = kNegInf;
-    int bt = INT_MAX;
-#pragma unroll
-    for (int i = 0; i < NV4; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int j = 4 * (tid + kTopkThreads * i) + c;
-        if (j < V && !((taken >> (4 * i + c)) & 1ull)) {
-          const float sc = __fadd_rn(plp, __fsub_rn(v[4 * i + c], lse));
-          if (bt == INT_MAX || better2(sc, j, bs, bt)) {
-            bs = sc;
-            bt = j;
-          }
-        }
-      }
-    block_best(bs, bt, red_f, red_i);
-    if (tid == 0) {
-      b.cand_score[static_cast<long long>(r) * b.B + k] = bs;
-      b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
-    }
-    if (((bt >> 2) % kTopkThreads) == tid) taken |= 1ull << (4 * ((bt >> 2) / kTopkThreads) + (bt & 3));
-  }
 }
 
 }  // namespace
@@ -861,32 +584,6 @@ void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv
   const size_t smem = sizeof(float) * (d + 33 + heads * (dh + max_src));
   launch_k(dec_cross_attention_kernel, max_rows, heads * 32, smem, st, 
       cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows, max_src, d, dh, scale, ctx, ldc, op);
-  MTG_CUDA(cudaGetLastError());
-}
-
-template <int NV4>
-static void launch_topk_nv(const float* logits, long long ldl, const BeamDev& b,
-                           cudaStream_t st) {
-  launch_k(topk_kernel<NV4>, b.R_max, kTopkThreads, 0, st, logits, ldl, b);
-}
-
-void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st) {
-  const int per = 4 * kTopkThreads;
-  const int nv4 = (b.V + per - 1) / per;
-  if (ldl % 4 != 0) fail(kStateError, "topk: logits pitch must be a multiple of 4");
-  if (b.B > kMaxBeam) fail(kUsageError, "beam size above 16 is not supported");
-  if (nv4 <= 1)
-    launch_topk_nv<1>(logits, ldl, b, st);
-  else if (nv4 <= 2)
-    launch_topk_nv<2>(logits, ldl, b, st);
-  else if (nv4 <= 4)
-    launch_topk_nv<4>(logits, ldl, b, st);
-  else if (nv4 <= 8)
-    launch_topk_nv<8>(logits, ldl, b, st);
-  else if (nv4 <= 16)
-    launch_topk_nv<16>(logits, ldl, b, st);
-  else
-    fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
   MTG_CUDA(cudaGetLastError());
 }
 

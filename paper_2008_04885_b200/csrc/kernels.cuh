@@ -9,7 +9,7 @@
 namespace mtg {
 
 constexpr int kMaxBeam = 16;
-constexpr int kTopkThreads = 512;
+constexpr int kTopkThreads = 1024;
 
 // Destination of a row's GEMM operand (the next linear layer's A matrix):
 // int8 + per-row scale (quant.cpp:108-122), bf16, or fp32 hi/lo (3xTF32).
@@ -120,8 +120,10 @@ struct BeamDev {
 void launch_beam_init(const BeamDev& b, cudaStream_t st);
 
 // log_softmax_row + candidate scores + per-row top-min(B,V) by (score desc,
-// token asc); one 512-thread CTA per live row, logits held in registers.
-// Supports V <= 32768.
+// token asc); one 1024-thread CTA per live row, logits held in registers
+// (topk.cu). The logits pitch must be topk_pitch(V) with the pad columns
+// set to -inf. Supports V <= 32768.
+long long topk_pitch(int V);
 void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st);
 
 // Per-sentence selection of beam_size candidates by (score desc, parent asc,

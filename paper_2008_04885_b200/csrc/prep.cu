@@ -162,7 +162,21 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, long long ld_x, i
   }
 }
 
+__global__ void fill_kernel(float* __restrict__ p, long long n, float value) {
+  pdl_wait();
+  pdl_trigger();
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = value;
+}
+
 }  // namespace
+
+void launch_fill(float* p, long long n, float value, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_k(fill_kernel, 1184, 256, 0, st, p, n, value);
+  MTG_CUDA(cudaGetLastError());
+}
 
 void launch_quantize_segments(const float* x, long long ld_x, int k, const int* seg_off,
                               int n_seg, const int* d_n_seg, int8_t* q, int k_pad,

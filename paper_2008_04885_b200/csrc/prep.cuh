@@ -27,6 +27,9 @@ void launch_quantize_rows(const float* x, long long ld_x, int k, int max_rows,
 void launch_cast_bf16(const float* x, long long ld_x, int k, int max_rows,
                       const int* d_rows, __nv_bfloat16* out, int k_pad, cudaStream_t st);
 
+// p[0..n) = value.
+void launch_fill(float* p, long long n, float value, cudaStream_t st);
+
 // hi = tf32(x) (round to nearest), lo = x - hi.
 void launch_split_tf32(const float* x, long long ld_x, int k, int max_rows,
                        const int* d_rows, float* hi, float* lo, int k_pad,
