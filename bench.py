@@ -237,15 +237,32 @@ def run_gpu(args):
             if rc == 0:
                 kern[name] = dict(ms=ms.value, bytes=by.value, flops=fl.value)
         g = kern["logits_gemm"]
-        tc_frac_peak = tc_peak * (2.0 if prec == mt.INT8 else 1.0)
+        ncu = {}
+        try:
+            ncu = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu.json")))
+        except OSError:
+            pass
+        measured = ncu.get("peaks_measured", {})
+        if prec == mt.INT8:
+            tc_frac_peak = measured.get("int8_tops", 2.0 * tc_peak)
+            src = ("int8 dense s8 TOPS measured by tools/peaks.py (torch._int_mm 8192^3), "
+                   "profiles/r01_ncu.json; MEASURED_PEAKS.json has no int8 entry")
+        elif prec == mt.F32:
+            tc_frac_peak = measured.get("tf32_tflops", tc_peak)
+            src = ("tf32 dense TFLOP/s measured by tools/peaks.py (profiles/r01_ncu.json); "
+                   "achieved counts the 3 tf32 MMAs of 3xTF32")
+        else:
+            tc_frac_peak = tc_peak
+            src = "MEASURED_PEAKS.json bf16_tflops (burst)"
+        nk = ncu.get("kernels", {}).get("logits_gemm_" + args.precision)
+        traffic = (nk["dram_read_bytes"] + nk["dram_write_bytes"]) if nk else None
+        achieved = g["flops"] / (g["ms"] * 1e-3) / 1e12
         extra["roofline"] = {
             "kernel": "logits_gemm (tcgen05 output projection, R=320 x V=32000 x K=512)",
-            "bound": "tensor", "achieved": g["flops"] / (g["ms"] * 1e-3) / 1e12,
-            "peak": tc_frac_peak, "unit": "TFLOP/s",
-            "frac": g["flops"] / (g["ms"] * 1e-3) / 1e12 / tc_frac_peak, "traffic": None,
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" + (
-                " x2 for int8 (dense int8 = 2x bf16 on sm_100)" if prec == mt.INT8 else "") +
-            (" ; fp32 counts 3 MMAs (3xTF32) vs the bf16 peak" if prec == mt.F32 else "")}
+            "bound": "tensor", "achieved": achieved, "peak": tc_frac_peak,
+            "unit": "TFLOP/s",  # int8: tera-ops (2 per multiply-add)
+            "frac": achieved / tc_frac_peak, "traffic": traffic,
+            "algorithmic_bytes": g["bytes"], "peak_source": src}
         extra["kernels"] = {
             k: dict(ms=v["ms"], gbs=v["bytes"] / (v["ms"] * 1e-3) / 1e9,
                     hbm_frac=v["bytes"] / (v["ms"] * 1e-3) / 1e9 / hbm_peak,

@@ -1,0 +1,261 @@
+// minimt_gpu.hpp -- header-only C++ shim over the C ABI (minimt_gpu.h) that
+// re-exposes the reference's decode API (proj/include/minimt/decode.hpp,
+// model.hpp, errors.hpp) so callers of minimt::beam_search /
+// translate_corpus switch by changing the namespace and the executor type:
+//
+//   minimt::F32Executor ex(model);                 // reference
+//   minimt::gpu::GpuExecutor ex(path, MTG_PREC_F32);  // this library
+//   Hypothesis h = beam_search(ex, src_ids, {}, cfg);
+//
+// Error behaviour mirrors errors.hpp: status codes are rethrown as the same
+// exception types. The text layer (Vocabulary, tokenize) stays host-side; the
+// id-level batched entry point is translate_ids().
+#ifndef MINIMT_GPU_HPP_
+#define MINIMT_GPU_HPP_
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "minimt_gpu.h"
+
+namespace minimt {
+namespace gpu {
+
+// ---- errors.hpp:8-34 --------------------------------------------------------
+struct ShapeError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ValueError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IndexError : std::out_of_range { using std::out_of_range::out_of_range; };
+struct StateError : std::logic_error { using std::logic_error::logic_error; };
+struct FormatError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct UsageError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IoError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+[[noreturn]] inline void throw_status(int rc, const std::string& msg) {
+  switch (rc) {
+    case MTG_SHAPE_ERROR: throw ShapeError(msg);
+    case MTG_VALUE_ERROR: throw ValueError(msg);
+    case MTG_INDEX_ERROR: throw IndexError(msg);
+    case MTG_STATE_ERROR: throw StateError(msg);
+    case MTG_FORMAT_ERROR: throw FormatError(msg);
+    case MTG_USAGE_ERROR: throw UsageError(msg);
+    case MTG_IO_ERROR: throw IoError(msg);
+    default: throw CudaError(msg);
+  }
+}
+inline void check(int rc) {
+  if (rc != MTG_OK) throw_status(rc, mtg_last_error());
+}
+
+constexpr int kPadId = 0, kUnkId = 1, kBosId = 2, kEosId = 3;  // model.hpp:16-19
+
+// ---- decode.hpp:15-31 ----------------------------------------------------------
+struct Hypothesis {
+  std::vector<int> tokens;
+  float logprob = 0.0f;
+  bool finished = false;
+  bool truncated = false;
+  float normalized = 0.0f;  // normalized_score(alpha) as computed on device
+  float normalized_score(float alpha) const {
+    const float len = static_cast<float>(tokens.size()) + 1.0f;
+    return logprob / std::pow((5.0f + len) / 6.0f, alpha);
+  }
+};
+
+struct BeamConfig {
+  int beam_size = 4;
+  int max_len = 64;
+  float length_penalty_alpha = 1.0f;
+};
+
+// ---- the Executor plugin point (model.hpp:113-171) -----------------------------
+// Owns a device-resident model. MTG_PREC_F32 ~ F32Executor, MTG_PREC_INT8 ~
+// Int8Executor (int8 files always decode int8), MTG_PREC_BF16 extension.
+class GpuExecutor {
+ public:
+  GpuExecutor(const std::string& sqnt_path, int precision, int device = 0) {
+    check(mtg_model_load(sqnt_path.c_str(), precision, device, &m_));
+  }
+  GpuExecutor(const std::string& config_json, uint64_t seed, int precision, int device = 0) {
+    check(mtg_model_create(config_json.c_str(), seed, precision, device, &m_));
+  }
+  ~GpuExecutor() { mtg_model_free(m_); }
+  GpuExecutor(const GpuExecutor&) = delete;
+  GpuExecutor& operator=(const GpuExecutor&) = delete;
+
+  mtg_model* handle() const { return m_; }
+  int precision() const { return mtg_model_precision(m_); }
+  std::string config_json() const {
+    std::string buf(4096, '\0');
+    check(mtg_model_config_json(m_, buf.data(), buf.size()));
+    return std::string(buf.c_str());
+  }
+  int max_seq_len() const {
+    const std::string j = config_json();
+    const auto p = j.find("\"max_seq_len\":");
+    return p == std::string::npos ? 128 : std::stoi(j.substr(p + 14));
+  }
+  void save(const std::string& path) const { check(mtg_model_save(m_, path.c_str())); }
+
+  // decode_step along a forced prefix (model.cpp:614-672): logits per step.
+  std::vector<float> forced_logits(const std::vector<int>& src,
+                                   const std::vector<int>& forced) const {
+    const int64_t off[2] = {0, static_cast<int64_t>(src.size())};
+    std::string cfg = config_json();
+    const auto p = cfg.find("\"tgt_vocab_size\":");
+    const int V = std::stoi(cfg.substr(p + 17));
+    std::vector<float> out(forced.size() * static_cast<size_t>(V));
+    check(mtg_forced_logits(m_, src.data(), off, 1, forced.data(),
+                            static_cast<int>(forced.size()), out.data()));
+    return out;
+  }
+
+ private:
+  mtg_model* m_ = nullptr;
+};
+
+// Batched id-level search: one call, many sentences (each ending with EOS).
+// Per-sentence failures come back as empty hypotheses with status != 0.
+struct BatchResult {
+  std::vector<Hypothesis> hyps;
+  std::vector<int> status;
+};
+
+inline BatchResult translate_ids(const GpuExecutor& ex,
+                                 const std::vector<std::vector<int>>& sources,
+                                 const BeamConfig& config, int max_batch = 0) {
+  std::vector<int32_t> ids;
+  std::vector<int64_t> off{0};
+  for (const auto& s : sources) {
+    ids.insert(ids.end(), s.begin(), s.end());
+    off.push_back(static_cast<int64_t>(ids.size()));
+  }
+  const int n = static_cast<int>(sources.size());
+  const int T = ex.max_seq_len();
+  std::vector<int32_t> toks(static_cast<size_t>(std::max(n, 1)) * T), len(std::max(n, 1)),
+      status(std::max(n, 1));
+  std::vector<float> lp(std::max(n, 1)), norm(std::max(n, 1));
+  std::vector<uint32_t> flags(std::max(n, 1));
+  mtg_beam_config c{config.beam_size, config.max_len, config.length_penalty_alpha, max_batch};
+  check(mtg_translate(ex.handle(), ids.data(), off.data(), n, &c, toks.data(), T, len.data(),
+                      lp.data(), norm.data(), flags.data(), status.data()));
+  BatchResult r;
+  for (int i = 0; i < n; ++i) {
+    Hypothesis h;
+    h.tokens.assign(toks.begin() + static_cast<size_t>(i) * T,
+                    toks.begin() + static_cast<size_t>(i) * T + len[i]);
+    h.logprob = lp[i];
+    h.normalized = norm[i];
+    h.finished = flags[i] & MTG_HYP_FINISHED;
+    h.truncated = flags[i] & MTG_HYP_TRUNCATED;
+    r.hyps.push_back(std::move(h));
+    r.status.push_back(status[i]);
+  }
+  return r;
+}
+
+// decode.hpp:35-38. Factor streams and shortlists are not on the GPU path yet.
+inline Hypothesis beam_search(const GpuExecutor& ex, const std::vector<int>& src_ids,
+                              const std::vector<std::vector<int>>& factor_ids,
+                              const BeamConfig& config,
+                              const std::vector<int>* shortlist = nullptr) {
+  if (config.beam_size < 1) throw UsageError("beam_search: beam size >= 1");
+  if (src_ids.empty()) throw UsageError("beam_search: empty source");
+  if (!factor_ids.empty()) throw UsageError("source factors are not supported on the GPU path");
+  if (shortlist) throw UsageError("shortlists are not supported on the GPU path yet");
+  BatchResult r = translate_ids(ex, {src_ids}, config);
+  if (r.status[0] != MTG_OK) throw_status(r.status[0], "beam_search failed");
+  return r.hyps[0];
+}
+
+// ---- decode.hpp:81-113 ------------------------------------------------------------
+struct LatencyReport {
+  std::vector<double> durations_s;
+  long output_tokens = 0;
+  double total_time_s = 0.0;
+  int count() const { return static_cast<int>(durations_s.size()); }
+  double percentile_ms(double p) const {  // eval.cpp:120-128 nearest rank
+    if (durations_s.empty()) return 0.0;
+    std::vector<double> v = durations_s;
+    std::sort(v.begin(), v.end());
+    size_t rank = static_cast<size_t>(std::ceil(p / 100.0 * static_cast<double>(v.size())));
+    if (rank == 0) rank = 1;
+    return v[rank - 1] * 1000.0;
+  }
+  double p50_ms() const { return percentile_ms(50.0); }
+  double p90_ms() const { return percentile_ms(90.0); }
+  double mean_ms() const {
+    if (durations_s.empty()) return 0.0;
+    double s = 0.0;
+    for (double d : durations_s) s += d;
+    return s / static_cast<double>(durations_s.size()) * 1000.0;
+  }
+  double tokens_per_sec() const { return total_time_s > 0.0 ? output_tokens / total_time_s : 0.0; }
+};
+
+using Clock = std::function<double()>;
+inline Clock steady_clock_seconds() {
+  return [] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  };
+}
+
+// translate_corpus on ids (decode.cpp:363-419 after tokenisation): sequential
+// batch-1 mode records per-sentence latency; batch_sentences > 1 runs
+// length-bucketed device batches and records only the total time. Failed
+// sentences yield empty hypotheses, like the reference's empty lines.
+inline std::vector<Hypothesis> translate_corpus_ids(const GpuExecutor& ex,
+                                                    const std::vector<std::vector<int>>& words,
+                                                    const BeamConfig& beam,
+                                                    LatencyReport* report = nullptr,
+                                                    int batch_sentences = 1, Clock clock = {}) {
+  if (!clock) clock = steady_clock_seconds();
+  const int msl = ex.max_seq_len();
+  std::vector<std::vector<int>> srcs;
+  for (const auto& w : words) {  // translate_one: append EOS, truncate keeping EOS
+    std::vector<int> s = w;
+    s.push_back(kEosId);
+    if (static_cast<int>(s.size()) > msl) {
+      s.resize(msl - 1);
+      s.push_back(kEosId);
+    }
+    srcs.push_back(std::move(s));
+  }
+  BeamConfig cfg = beam;  // max_len <= 0: derived per sentence on device
+  std::vector<Hypothesis> out(srcs.size());
+  if (batch_sentences > 1) {
+    const double t0 = clock();
+    BatchResult r = translate_ids(ex, srcs, cfg, batch_sentences);
+    for (size_t i = 0; i < srcs.size(); ++i)
+      if (r.status[i] == MTG_OK) out[i] = r.hyps[i];
+    if (report) {
+      report->total_time_s += clock() - t0;
+      for (const auto& h : out) report->output_tokens += static_cast<long>(h.tokens.size());
+    }
+    return out;
+  }
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    const double t0 = clock();
+    BatchResult r = translate_ids(ex, {srcs[i]}, cfg);
+    if (r.status[0] == MTG_OK) out[i] = r.hyps[0];
+    const double dt = clock() - t0;
+    if (report) {
+      report->durations_s.push_back(dt);
+      report->total_time_s += dt;
+      report->output_tokens += static_cast<long>(out[i].tokens.size());
+    }
+  }
+  return out;
+}
+
+}  // namespace gpu
+}  // namespace minimt
+
+#endif  // MINIMT_GPU_HPP_
