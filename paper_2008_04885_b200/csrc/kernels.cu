@@ -284,23 +284,46 @@ __device__ __forceinline__ float reduce_scatter32(float (&a)[32]) {
   return a[0];
 }
 
-// One query against n keys, one warp. q: dh floats in smem; s: n floats of
-// per-warp smem scratch. P3 dots, P1 sums (softmax denominator and context).
-template <bool kVecKeys = true, class KP, class VP>
-__device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float scale, KP kp,
+// Shared-memory float4 load the compiler cannot hoist out of the key loop
+// (keeping q in registers would spill at the 80-register occupancy target).
+__device__ __forceinline__ float4 lds_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+// One query against n keys, one warp. q: dh floats in smem (16-byte aligned);
+// s: n floats of per-warp smem scratch. P3 dots, P1 sums (softmax denominator
+// and context). DH > 0 fixes the head dim at compile time (float4 paths, all
+// of a key row's loads issued before its dot product); DH == 0 is generic.
+// Key/value rows must be 16-byte aligned when DH % 4 == 0.
+template <int DH, class KP, class VP>
+__device__ __forceinline__ void attend_warp(const float* q, int n, int dh_rt, float scale, KP kp,
                                             VP vp, float* s, float* out) {
   const int lane = threadIdx.x & 31;
+  const int dh = DH > 0 ? DH : dh_rt;
+  constexpr bool kVec = DH > 0 && DH % 4 == 0;
   float mx = kNegInf;
   for (int j = lane; j < n; j += 32) {
     const float* k = kp(j);
     float acc = 0.0f;
-    if (kVecKeys && (dh & 3) == 0) {
-      for (int c = 0; c < dh; c += 4) {
-        const float4 kv = *reinterpret_cast<const float4*>(k + c);
-        acc = __fadd_rn(acc, __fmul_rn(q[c], kv.x));
-        acc = __fadd_rn(acc, __fmul_rn(q[c + 1], kv.y));
-        acc = __fadd_rn(acc, __fmul_rn(q[c + 2], kv.z));
-        acc = __fadd_rn(acc, __fmul_rn(q[c + 3], kv.w));
+    if constexpr (kVec) {
+      constexpr int G = DH / 4 < 16 ? DH / 4 : 16;  // float4 loads in flight per group
+#pragma unroll
+      for (int g = 0; g < DH / 4; g += G) {
+        float4 kv[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) kv[i] = *reinterpret_cast<const float4*>(k + 4 * (g + i));
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          const float4 qv = lds_f4(q + 4 * (g + i));
+          acc = __fadd_rn(acc, __fmul_rn(qv.x, kv[i].x));
+          acc = __fadd_rn(acc, __fmul_rn(qv.y, kv[i].y));
+          acc = __fadd_rn(acc, __fmul_rn(qv.z, kv[i].z));
+          acc = __fadd_rn(acc, __fmul_rn(qv.w, kv[i].w));
+        }
       }
     } else {
       for (int c = 0; c < dh; ++c) acc = __fadd_rn(acc, __fmul_rn(q[c], k[c]));
@@ -322,30 +345,34 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
   // Context: lanes own keys j = lane + 32u and accumulate p_j * v_j[c] for a
   // 32-column chunk, then a reduce-scatter butterfly leaves column c0+lane in
   // lane `lane` (per column the same tree as the P1 warp sum).
-  for (int c0 = 0; c0 < dh; c0 += 32) {
+#pragma unroll 1
+  for (int c0 = 0; c0 < (DH > 0 ? DH : 4096); c0 += 32) {
+    if (DH == 0 && c0 >= dh) break;
     float acc[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
-    const bool full = kVecKeys && c0 + 32 <= dh && (dh & 3) == 0;
     for (int j = lane; j < n; j += 32) {
       const float p = s[j];
       const float* v = vp(j) + c0;
-      float vv[32];
-      if (full) {
+      if constexpr (kVec && DH % 32 == 0) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 f = *reinterpret_cast<const float4*>(v + i);
-          vv[i] = f.x;
-          vv[i + 1] = f.y;
-          vv[i + 2] = f.z;
-          vv[i + 3] = f.w;
+        for (int g = 0; g < 32; g += 16) {
+          float4 f[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) f[i] = *reinterpret_cast<const float4*>(v + g + 4 * i);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            acc[g + 4 * i] = __fadd_rn(acc[g + 4 * i], __fmul_rn(p, f[i].x));
+            acc[g + 4 * i + 1] = __fadd_rn(acc[g + 4 * i + 1], __fmul_rn(p, f[i].y));
+            acc[g + 4 * i + 2] = __fadd_rn(acc[g + 4 * i + 2], __fmul_rn(p, f[i].z));
+            acc[g + 4 * i + 3] = __fadd_rn(acc[g + 4 * i + 3], __fmul_rn(p, f[i].w));
+          }
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) vv[i] = c0 + i < dh ? v[i] : 0.0f;
+        for (int i = 0; i < 32; ++i)
+          acc[i] = __fadd_rn(acc[i], __fmul_rn(p, c0 + i < dh ? v[i] : 0.0f));
       }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(p, vv[i]));
     }
     const float col = reduce_scatter32(acc);
     if (c0 + lane < dh) out[c0 + lane] = col;
@@ -353,35 +380,51 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh, float
   __syncwarp();
 }
 
+__host__ __device__ constexpr int enc_kv_pitch(int dh) { return dh % 4 == 0 ? dh + 4 : dh + 1; }
+
+// Encoder self-attention (model.cpp:418-470 / attention): CTA per (sentence,
+// head). K and V are staged once in smem (row pitch dh+4: conflict-free
+// float4 reads with lane = key); warps take queries round-robin.
+template <int DH>
 __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ldq,
-                                     const int* __restrict__ off, int d, int dh, int max_len,
+                                     const int* __restrict__ off, int d, int dh_rt, int max_len,
                                      float scale, float* __restrict__ ctx, long long ldc) {
   pdl_wait();
   pdl_trigger();
-  // K and V of this (sentence, head) are staged once in smem with coalesced
-  // loads; K rows are padded to dh+1 floats (lane j reads key row j).
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) float sm[];
+  const int dh = DH > 0 ? DH : dh_rt;
+  const int P = enc_kv_pitch(dh);
   const int s = blockIdx.x, h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int r0 = off[s], n = off[s + 1] - r0;
   float* Ks = sm;
-  float* Vs = Ks + max_len * (dh + 1);
-  float* qs = Vs + max_len * dh + warp * (dh + max_len);
-  float* ss = qs + dh;
+  float* Vs = Ks + max_len * P;
+  float* qs = Vs + max_len * P + warp * (P + ((max_len + 3) & ~3));
+  float* ss = qs + P;
   const float* base = qkv + static_cast<long long>(r0) * ldq + h * dh;
-  for (int idx = threadIdx.x; idx < n * dh; idx += blockDim.x) {
-    const int j = idx / dh, c = idx - j * dh;
-    Ks[j * (dh + 1) + c] = base[j * ldq + d + c];
-    Vs[j * dh + c] = base[j * ldq + 2 * d + c];
+  if constexpr (DH > 0 && DH % 4 == 0) {
+    constexpr int Q4 = DH / 4;
+    for (int idx = threadIdx.x; idx < n * Q4; idx += blockDim.x) {
+      const int j = idx / Q4, c = 4 * (idx - j * Q4);
+      *reinterpret_cast<float4*>(Ks + j * P + c) =
+          *reinterpret_cast<const float4*>(base + j * ldq + d + c);
+      *reinterpret_cast<float4*>(Vs + j * P + c) =
+          *reinterpret_cast<const float4*>(base + j * ldq + 2 * d + c);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < n * dh; idx += blockDim.x) {
+      const int j = idx / dh, c = idx - j * dh;
+      Ks[j * P + c] = base[j * ldq + d + c];
+      Vs[j * P + c] = base[j * ldq + 2 * d + c];
+    }
   }
   __syncthreads();
   for (int i = warp; i < n; i += nw) {
     for (int c = lane; c < dh; c += 32) qs[c] = base[i * ldq + c];
     __syncwarp();
-    attend_warp<false>(
-        qs, n, dh, scale, [&](int j) { return Ks + j * (dh + 1); },
-        [&](int j) { return Vs + j * dh; }, ss,
-        ctx + static_cast<long long>(r0 + i) * ldc + h * dh);
+    attend_warp<DH>(
+        qs, n, dh, scale, [&](int j) { return Ks + j * P; }, [&](int j) { return Vs + j * P; },
+        ss, ctx + static_cast<long long>(r0 + i) * ldc + h * dh);
   }
 }
 
@@ -412,65 +455,74 @@ __device__ __forceinline__ void finish_ctx_row(const float* row, int d, long lon
   write_operand(op, r, row, d, qscale_of(red[32]), tid, blockDim.x);
 }
 
+__host__ __device__ constexpr int round4(int x) { return (x + 3) & ~3; }
+
+// Decoder self-attention over the cached prefix (model.cpp:620-660): CTA per
+// hypothesis row, warp per head; key j of row r lives at cache row
+// anc[r][j] of step j. Smem: per-head [q | scores] blocks (16-byte aligned),
+// then the context row, the reduction scratch and the ancestor row.
+template <int DH>
 __global__ void __launch_bounds__(256, 3)
     dec_self_attention_kernel(const float* __restrict__ cache, int r_max, int T,
-                                          const int* __restrict__ anc0,
-                                          const int* __restrict__ anc1, const int* d_rows,
-                                          const int* d_step, int d, int dh, float scale,
-                                          float* __restrict__ ctx, long long ldc, OperandOut op) {
+                              const int* __restrict__ anc0, const int* __restrict__ anc1,
+                              const int* d_rows, const int* d_step, int d, int dh_rt, float scale,
+                              float* __restrict__ ctx, long long ldc, OperandOut op) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
+  const int dh = DH > 0 ? DH : dh_rt;
   const int t = *d_step;
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* row = sm;                                   // [d] context row
-  float* red = row + d;                              // [33]
-  int* arow = reinterpret_cast<int*>(red + 33);      // [T] ancestor rows
-  float* qs = reinterpret_cast<float*>(arow + T) + h * (dh + T);
-  float* ss = qs + dh;
+  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31, heads = blockDim.x >> 5;
+  const int W = round4(dh) + round4(T);
+  float* qs = sm + h * W;
+  float* ss = qs + round4(dh);
+  float* row = sm + heads * W;                   // [d] context row
+  float* red = row + d;                          // [33]
+  int* arow = reinterpret_cast<int*>(red + 33);  // [T] ancestor rows
   const int* ar = ((t & 1) ? anc1 : anc0) + static_cast<long long>(r) * T;
   for (int j = threadIdx.x; j <= t; j += blockDim.x) arow[j] = ar[j];
   const long long ld3 = 3LL * d;
   const float* q = cache + (static_cast<long long>(t) * r_max + r) * ld3 + h * dh;
   for (int c = lane; c < dh; c += 32) qs[c] = q[c];
   __syncthreads();
-  attend_warp(
+  const float* kb = cache + d + h * dh;
+  attend_warp<DH>(
       qs, t + 1, dh, scale,
-      [&](int j) { return cache + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d + h * dh; },
-      [&](int j) {
-        return cache + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + 2 * d + h * dh;
-      },
-      ss, row + h * dh);
+      [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; },
+      [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d; }, ss,
+      row + h * dh);
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
 
+// Decoder cross-attention over the sentence's encoder keys/values.
+template <int DH>
 __global__ void __launch_bounds__(256, 3)
     dec_cross_attention_kernel(const float* __restrict__ cq, long long ldq,
-                                           const float* __restrict__ ckv,
-                                           const int* __restrict__ row_sent,
-                                           const int* __restrict__ enc_off,
-                                           const int* __restrict__ enc_len, const int* d_rows,
-                                           int max_src, int d, int dh, float scale,
-                                           float* __restrict__ ctx, long long ldc, OperandOut op) {
+                               const float* __restrict__ ckv, const int* __restrict__ row_sent,
+                               const int* __restrict__ enc_off, const int* __restrict__ enc_len,
+                               const int* d_rows, int max_src, int d, int dh_rt, float scale,
+                               float* __restrict__ ctx, long long ldc, OperandOut op) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dh = DH > 0 ? DH : dh_rt;
+  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31, heads = blockDim.x >> 5;
   const int s = row_sent[r];
   const float* kv = ckv + static_cast<long long>(enc_off[s]) * 2 * d + h * dh;
   const int n = enc_len[s];
-  float* row = sm;
+  const int W = round4(dh) + round4(max_src);
+  float* qs = sm + h * W;
+  float* ss = qs + round4(dh);
+  float* row = sm + heads * W;
   float* red = row + d;
-  float* qs = red + 33 + h * (dh + max_src);
-  float* ss = qs + dh;
   for (int c = lane; c < dh; c += 32) qs[c] = cq[r * ldq + h * dh + c];
   __syncwarp();
-  attend_warp(
+  attend_warp<DH>(
       qs, n, dh, scale, [&](int j) { return kv + static_cast<long long>(j) * 2 * d; },
       [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; }, ss, row + h * dh);
   __syncthreads();
@@ -545,19 +597,21 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
   if (n_sent <= 0) return;
   const int dh = d / heads;
   const int nw = 8;
+  const int P = enc_kv_pitch(dh);
   const size_t smem =
-      sizeof(float) * (size_t(max_len) * (2 * dh + 1) + size_t(nw) * (dh + max_len));
-  static size_t configured = 48 * 1024;
+      sizeof(float) * (size_t(max_len) * 2 * P + size_t(nw) * (P + round4(max_len)));
   if (smem > 227 * 1024)
     fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
-  if (smem > configured) {
-    MTG_CUDA(cudaFuncSetAttribute(enc_attention_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
+  static size_t configured[2] = {48 * 1024, 48 * 1024};
+  size_t& cfg = configured[dh == 64 ? 0 : 1];
+  if (smem > cfg) {
+    MTG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    configured = smem;
+    cfg = smem;
   }
-  launch_k(enc_attention_kernel, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len,
-                                                                   scale, ctx, ldc);
+  launch_k(k, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale, ctx,
+           ldc);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -567,10 +621,11 @@ void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const i
                                const OperandOut& op, cudaStream_t st) {
   if (r_max <= 0) return;
   const int dh = d / heads;
-  const size_t smem = sizeof(float) * (d + 33 + T + heads * (dh + T));
-  launch_k(dec_self_attention_kernel, r_max, heads * 32, smem, st, qkv_cache, r_max, T, anc0, anc1,
-                                                             d_rows, d_step, d, dh, scale, ctx,
-                                                             ldc, op);
+  if (heads > 32) fail(kUsageError, "attention: at most 32 heads");
+  const size_t smem = sizeof(float) * (size_t(heads) * (round4(dh) + round4(T)) + d + 33 + T);
+  auto k = dh == 64 ? dec_self_attention_kernel<64> : dec_self_attention_kernel<0>;
+  launch_k(k, r_max, heads * 32, smem, st, qkv_cache, r_max, T, anc0, anc1, d_rows, d_step, d, dh,
+           scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -581,9 +636,11 @@ void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv
                                 cudaStream_t st) {
   if (max_rows <= 0) return;
   const int dh = d / heads;
-  const size_t smem = sizeof(float) * (d + 33 + heads * (dh + max_src));
-  launch_k(dec_cross_attention_kernel, max_rows, heads * 32, smem, st, 
-      cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows, max_src, d, dh, scale, ctx, ldc, op);
+  if (heads > 32) fail(kUsageError, "attention: at most 32 heads");
+  const size_t smem = sizeof(float) * (size_t(heads) * (round4(dh) + round4(max_src)) + d + 33);
+  auto k = dh == 64 ? dec_cross_attention_kernel<64> : dec_cross_attention_kernel<0>;
+  launch_k(k, max_rows, heads * 32, smem, st, cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows,
+           max_src, d, dh, scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
 }
 
