@@ -154,6 +154,11 @@ void* mtg_model_stream(const mtg_model* m);
 int mtg_time_kernel(mtg_model* m, int kernel, int iters, float* ms_per_launch,
                     double* bytes_per_launch, double* flops_per_launch);
 
+/* Diagnostics: with MTG_DIAG_EVENTS=1 in the environment, the decode-step graph
+ * records an event after every kernel (serialising them) and this returns the
+ * per-kernel average step times of the last translate call as text. */
+int mtg_diag_report(mtg_model* m, char* buf, size_t buf_size);
+
 #ifdef __cplusplus
 }
 #endif

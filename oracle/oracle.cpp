@@ -4,9 +4,13 @@
 // this file agree on the ones below):
 //   P1 lane sum     : 32 partials, partial l = sum of v[l], v[l+32], ... in
 //                     order, then xor-butterfly (16,8,4,2,1). (warp_sum)
-//   P2 block sum    : 1024 partials, partial t = sum over i of v[4(t+1024i)+c],
-//                     c = 0..3, in order; P1 butterfly per 32-thread warp, then
-//                     P1 butterfly across the 32 warp sums. (block_sum_1024)
+//   P6 log-sum-exp  : per 32-column slice k: m_k = max, s_k = sum in column
+//                     order of exp(x - m_k) (0 if m_k = -inf); M = max m_k;
+//                     S = sum over k of s_k * exp(m_k - M) (0 if m_k = -inf):
+//                     128 partials (t sums k = t + 128 i), P1 butterfly per
+//                     32, then (W0 + W1) + (W2 + W3);
+//                     lse = log(S) + M. (log_softmax_row; the GPU computes the
+//                     slices in the output-projection GEMM epilogue)
 //   P3 dot          : acc = 0; acc = acc + a[c]*b[c] for c ascending (no FMA).
 //   attention ctx   : ctx[c] = P1 sum over keys j of p_j * v_j[c].
 //   P4 exp/log/pow  : detmath.h.
@@ -676,31 +680,6 @@ float warp_sum(const float* v, Index n) {
   return p[0];
 }
 
-float butterfly32(float* p) {
-  for (int off = 16; off > 0; off >>= 1) {
-    float t[32];
-    for (int l = 0; l < 32; ++l) t[l] = p[l] + p[l ^ off];
-    std::memcpy(p, t, 32 * sizeof(float));
-  }
-  return p[0];
-}
-
-// P2 (1024 threads = 32 warps; the 32 warp sums are butterflied in one warp).
-float block_sum_1024(const float* v, Index n) {
-  constexpr int kT = 1024;
-  static thread_local std::vector<float> part(kT);
-  for (int t = 0; t < kT; ++t) {
-    float s = 0.0f;
-    for (Index base = 4LL * t; base < n; base += 4LL * kT)
-      for (int c = 0; c < 4; ++c)
-        if (base + c < n) s = s + v[base + c];
-    part[t] = s;
-  }
-  float ws[32];
-  for (int w = 0; w < 32; ++w) ws[w] = w < kT / 32 ? butterfly32(&part[w * 32]) : 0.0f;
-  return butterfly32(ws);
-}
-
 // P3
 inline float dot_seq(const float* a, const float* b, Index n) {
   float acc = 0.0f;
@@ -1099,13 +1078,50 @@ float Hypothesis::normalized_score(float alpha) const {
   return logprob / orc_powf((5.0f + len) / 6.0f, alpha);
 }
 
-// decode.cpp:25-30 in the P2 order: mx; lse = log(sum exp(x - mx)) + mx.
+// decode.cpp:25-30 in the P6 order: lse = log(sum exp(x - max)) + max, the sum
+// taken per 32-column slice against the slice max and then rescaled.
 std::vector<float> log_softmax_row(const float* x, int n) {
-  float mx = -INFINITY;
-  for (int j = 0; j < n; ++j) mx = std::max(mx, x[j]);
+  const int nsub = (n + 31) / 32;
+  std::vector<float> u(static_cast<size_t>(nsub));
+  std::vector<float> m(static_cast<size_t>(nsub));
+  float M = -INFINITY;
+  for (int k = 0; k < nsub; ++k) {
+    const int j0 = 32 * k, j1 = std::min(n, j0 + 32);
+    float best = -INFINITY;
+    bool any = false;
+    for (int j = j0; j < j1; ++j)
+      if (x[j] > best) {
+        best = x[j];
+        any = true;
+      }
+    float s = 0.0f;
+    if (any)
+      for (int j = j0; j < j1; ++j) s = s + orc_expf(x[j] - best);
+    m[k] = best;
+    u[k] = s;
+    M = std::max(M, best);
+  }
+  for (int k = 0; k < nsub; ++k) u[k] = m[k] == -INFINITY ? 0.0f : u[k] * orc_expf(m[k] - M);
+  // 128 thread partials (t sums k = t + 128 i), P1 butterfly per 32-thread
+  // warp, then (W0 + W1) + (W2 + W3).
+  float tp[128];
+  for (int t = 0; t < 128; ++t) {
+    float a = 0.0f;
+    for (int k = t; k < nsub; k += 128) a = a + u[k];
+    tp[t] = a;
+  }
+  float w[4];
+  for (int j = 0; j < 4; ++j) {
+    float* p = tp + 32 * j;
+    for (int off = 16; off > 0; off >>= 1) {
+      float tt[32];
+      for (int l = 0; l < 32; ++l) tt[l] = p[l] + p[l ^ off];
+      std::memcpy(p, tt, sizeof tt);
+    }
+    w[j] = p[0];
+  }
+  const float lse = orc_logf((w[0] + w[1]) + (w[2] + w[3])) + M;
   std::vector<float> e(static_cast<size_t>(n));
-  for (int j = 0; j < n; ++j) e[j] = orc_expf(x[j] - mx);
-  const float lse = orc_logf(block_sum_1024(e.data(), n)) + mx;
   for (int j = 0; j < n; ++j) e[j] = x[j] - lse;
   return e;
 }

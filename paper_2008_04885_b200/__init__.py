@@ -108,6 +108,7 @@ def _load():
     lib.mtg_translate_staged.argtypes = [c_void_p, c_void_p]
     lib.mtg_last_launch_count.argtypes = [c_void_p]
     lib.mtg_last_launch_count.restype = ctypes.c_int64
+    lib.mtg_diag_report.argtypes = [c_void_p, ctypes.c_char_p, ctypes.c_size_t]
     return lib
 
 
@@ -336,6 +337,12 @@ class Model:
 
     def last_launch_count(self) -> int:
         return int(_lib.mtg_last_launch_count(self._h))
+
+    def diag_report(self) -> str:
+        """Per-kernel decode-step times (needs MTG_DIAG_EVENTS=1 at model creation)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(_lib.mtg_diag_report(self._h, buf, len(buf)))
+        return buf.value.decode()
 
 
 def beam_search(model: Model, src_ids: Sequence[int], factor_ids=(), config: BeamConfig = None,

@@ -171,4 +171,16 @@ int mtg_time_kernel(mtg_model* m, int kernel, int iters, float* ms_per_launch,
   });
 }
 
+int mtg_diag_report(mtg_model* m, char* buf, size_t buf_size) {
+  return guarded([&] {
+    Engine& e = engine(m);
+    std::lock_guard<std::mutex> lock(e.mutex());
+    const std::string r = e.diag_report();
+    if (!buf || buf_size == 0) fail(kUsageError, "diag_report: empty buffer");
+    const size_t n = std::min(buf_size - 1, r.size());
+    std::memcpy(buf, r.data(), n);
+    buf[n] = '\0';
+  });
+}
+
 }  // extern "C"

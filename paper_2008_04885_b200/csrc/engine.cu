@@ -2,6 +2,9 @@
 // and the device-resident beam-search loop (decode.cpp:34-109).
 #include "engine.hpp"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <functional>
@@ -153,6 +156,7 @@ Engine::Engine(HostModel model, int precision, int device)
   if (prec_ != kF32 && prec_ != kBF16 && prec_ != kINT8)
     fail(kUsageError, "unknown precision " + std::to_string(prec_));
   if (host_.quantized && prec_ != kINT8) prec_ = kINT8;  // tools/minimt.cpp:317-320
+  if (const char* e = std::getenv("MTG_DIAG_EVENTS")) diag_ = e[0] == '1';
   if (prec_ == kINT8 && !host_.quantized) quantize_weights(host_);
   const ModelConfig& c = host_.config;
   c.validate();
@@ -167,7 +171,8 @@ Engine::Engine(HostModel model, int precision, int device)
   d_ = c.d_model;
   dff_ = c.d_ff;
   V_ = c.tgt_vocab_size;
-  Vp_ = static_cast<int>(topk_pitch(V_));  // pad columns hold -inf (top-k)
+  Vp_ = static_cast<int>(topk_pitch(V_));
+  part_ld_ = softmax_part_pitch(V_);
   T_ = c.max_seq_len;
   heads_ = c.num_heads;
   upload_weights();
@@ -175,6 +180,7 @@ Engine::Engine(HostModel model, int precision, int device)
 
 Engine::~Engine() {
   cudaSetDevice(device_);
+  diag_clear();
   plan_cache(this).clear();
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);
@@ -276,11 +282,9 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   dec_ctx_.resize(r_max_ * d);
   dec_cq_.resize(r_max_ * d);
   logits_.resize(size_t(r_max_) * Vp_);
-  // The GEMM writes columns < V only; the pad stays -inf (adds exp(-inf) = 0
-  // to the log-softmax sum and never scores).
-  launch_fill(logits_.get(), static_cast<long long>(r_max_) * Vp_, -__builtin_huge_valf(),
-              stream_);
-  MTG_CUDA(cudaStreamSynchronize(stream_));
+  part_m_.resize(size_t(r_max_) * part_ld_);
+  part_s_.resize(size_t(r_max_) * part_ld_);
+  part_arg_.resize(size_t(r_max_) * part_ld_);
   qkv_cache_.clear();
   qkv_cache_.resize(c.num_decoder_layers);
   for (auto& b : qkv_cache_) b.resize(size_t(T_) * r_max_ * 3 * d);
@@ -323,6 +327,7 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   sel_parent_.resize(size_t(N) * B);
   sel_tok_.resize(size_t(N) * B);
   sel_lp_.resize(size_t(N) * B);
+  sel_count_.resize(1);
 
   BeamDev& b = beam_;
   b.step = step_.get();
@@ -355,6 +360,7 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   b.sel_parent = sel_parent_.get();
   b.sel_tok = sel_tok_.get();
   b.sel_lp = sel_lp_.get();
+  b.sel_count = sel_count_.get();
   b.N = N;
   b.B = B;
   b.T = T_;
@@ -383,7 +389,7 @@ void Engine::prep(const float* x, long long ldx, int k, int max_rows, const int*
     launch_split_tf32(x, ldx, k, max_rows, d_rows, out.hi.get(), out.lo.get(), out.k_pad,
                       stream_);
   }
-  count();
+  count("operand prep");
 }
 
 void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
@@ -409,7 +415,64 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   ep.d_M = d_m;
   ep.N = w.n;
   launch_gemm(it->second, ep, stream_);
-  count();
+  count(w.n == 3 * d_ ? "gemm qkv" : w.n == 2 * d_ ? "gemm kv" : w.n == dff_ ? "gemm w1"
+        : w.k == dff_ ? "gemm w2" : "gemm d x d");
+}
+
+void Engine::count(const char* tag) {
+  ++launches_;
+  if (diag_ && capturing_) {
+    diag_marks_.push_back({tag, nullptr});
+    MTG_CUDA(cudaEventCreate(&diag_marks_.back().ev));
+    MTG_CUDA(cudaEventRecordWithFlags(diag_marks_.back().ev, stream_, cudaEventRecordExternal));
+  }
+}
+
+void Engine::diag_clear() {
+  for (auto& m : diag_marks_)
+    if (m.ev) cudaEventDestroy(m.ev);
+  diag_marks_.clear();
+  diag_ms_.clear();
+  diag_steps_ = 0;
+}
+
+std::string Engine::diag_report() const {
+  std::string out = "steps " + std::to_string(diag_steps_) + "\n";
+  if (diag_steps_ == 0) return out;
+  double total = 0.0;
+  for (size_t i = 1; i < diag_ms_.size(); ++i) total += diag_ms_[i];
+  for (size_t i = 1; i < diag_ms_.size(); ++i) {
+    char line[160];
+    std::snprintf(line, sizeof line, "%3zu %-32s %8.2f us\n", i, diag_marks_[i].name.c_str(),
+                  1000.0 * diag_ms_[i] / diag_steps_);
+    out += line;
+  }
+  char tl[96];
+  std::snprintf(tl, sizeof tl, "total per step %.2f us\n", 1000.0 * total / diag_steps_);
+  return out + tl;
+}
+
+void Engine::gemm_logits(int m, const int* d_m) {
+  auto& cache = plan_cache(this);
+  PlanKey key{act_d_.op().ptr, logits_w_.op().ptr, m};
+  auto it = cache.find(key);
+  if (it == cache.end())
+    it = cache.emplace(key, plan_gemm(act_d_.op(), logits_w_.op(), m, logits_w_.n, 0, 128)).first;
+  GemmEpilogue ep{};
+  ep.C = logits_.get();
+  ep.ldc = Vp_;
+  ep.a_scale = act_d_.row_scale.get();
+  ep.w_seg_scale = logits_w_.seg_scale.get();
+  ep.seg_width = logits_w_.seg_width;
+  ep.M = m;
+  ep.d_M = d_m;
+  ep.N = logits_w_.n;
+  ep.part_m = part_m_.get();
+  ep.part_s = part_s_.get();
+  ep.part_arg = part_arg_.get();
+  ep.part_ld = part_ld_;
+  launch_gemm(it->second, ep, stream_);
+  count("logits gemm + softmax partials");
 }
 
 // Validates and uploads sources (translate_one / beam_search / embed_source
@@ -547,7 +610,7 @@ void Engine::decoder_body() {
   launch_embed_tgt(row_prev_.get(), dr, R, step_.get(), tgt_embed_f32_.get(),
                    prec_ == kINT8 ? tgt_embed_q_.get() : nullptr, tgt_scale_, d_, sqrt_d,
                    pe_.get(), dec_y_.get(), d, stream_);
-  count();
+  count("embed_tgt");
   // Decoder rows are their own quantization segments (one hypothesis row per
   // Executor::linear call in decode_step), so LayerNorm and attention write
   // the next GEMM's operand directly.
@@ -555,7 +618,7 @@ void Engine::decoder_body() {
   auto ln_dec = [&](const LN& ln) {
     launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), dec_a_.get(), d, nullptr,
                      &od, stream_);
-    count();
+    count("layernorm");
   };
   for (int l = 0; l < c.num_decoder_layers; ++l) {
     DecLayer& L = dec_[l];
@@ -564,14 +627,14 @@ void Engine::decoder_body() {
          static_cast<long long>(R) * 3 * d, step_.get());
     launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
                               step_.get(), d_, heads_, scale, dec_ctx_.get(), d, od, stream_);
-    count();
+    count("self attention");
     gemm(act_d_, L.self_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
     ln_dec(L.n2);
     gemm(act_d_, L.cross_q, R, dr, dec_cq_.get(), d, nullptr, nullptr, 0);
     launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
                                enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d, od,
                                stream_);
-    count();
+    count("cross attention");
     gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
     ln_dec(L.n3);
     gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
@@ -579,7 +642,7 @@ void Engine::decoder_body() {
     gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
   }
   ln_dec(dec_final_);
-  gemm(act_d_, logits_w_, R, dr, logits_.get(), Vp_, nullptr, nullptr, 0);
+  gemm_logits(R, dr);
 }
 
 void Engine::ensure_step_graph() {
@@ -595,21 +658,34 @@ void Engine::ensure_step_graph() {
   step_exec_ = nullptr;
   step_graph_ = nullptr;
   const int64_t before = launches_;
+  diag_clear();
   MTG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  capturing_ = true;
   try {
+    if (diag_) {
+      diag_marks_.push_back({"start", nullptr});
+      MTG_CUDA(cudaEventCreate(&diag_marks_.back().ev));
+      MTG_CUDA(cudaEventRecordWithFlags(diag_marks_.back().ev, stream_, cudaEventRecordExternal));
+    }
     decoder_body();
-    launch_topk(logits_.get(), Vp_, beam_, stream_);
+    launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
+                        part_ld_, beam_, stream_);
+    count("softmax + top-k merge");
     launch_beam_select(beam_, stream_);
+    count("beam select");
     launch_beam_reorder(beam_, stream_);
+    count("beam reorder");
   } catch (...) {
+    capturing_ = false;
     cudaGraph_t g = nullptr;
     cudaStreamEndCapture(stream_, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
+  capturing_ = false;
   MTG_CUDA(cudaStreamEndCapture(stream_, &step_graph_));
   MTG_CUDA(cudaGraphInstantiate(&step_exec_, step_graph_, 0));
-  step_kernels_ = launches_ - before + 3;
+  step_kernels_ = launches_ - before;
   launches_ = before;
   step_key_ = key;
 }
@@ -621,6 +697,16 @@ void Engine::decode_loop(int t_run) {
   for (int t = 0; t < t_run; ++t) {
     MTG_CUDA(cudaGraphLaunch(step_exec_, stream_));
     launches_ += step_kernels_;
+    if (diag_) {
+      MTG_CUDA(cudaStreamSynchronize(stream_));
+      diag_ms_.resize(diag_marks_.size(), 0.0);
+      for (size_t i = 1; i < diag_marks_.size(); ++i) {
+        float ms = 0.0f;
+        MTG_CUDA(cudaEventElapsedTime(&ms, diag_marks_[i - 1].ev, diag_marks_[i].ev));
+        diag_ms_[i] += ms;
+      }
+      ++diag_steps_;
+    }
     if ((t + 1) % 8 == 0 && t + 1 < t_run) {
       MTG_CUDA(cudaMemcpyAsync(h_pinned_, n_rows_.get(), sizeof(int), cudaMemcpyDeviceToHost,
                                stream_));
@@ -735,15 +821,18 @@ void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double
   std::function<void()> launch;
   if (kernel == 0) {  // decoder output projection (tied tgt_embed)
     launch = [&] {
-      gemm(act_d_, logits_w_, r_max_, scratch_rows_.get(), logits_.get(), Vp_, nullptr, nullptr, 0);
+      gemm_logits(r_max_, scratch_rows_.get());
     };
     *bytes = double(split) * eb * (double(V_) * logits_w_.k_pad + double(R) * act_d_.k_pad) +
              4.0 * R * V_;
     *flops = 2.0 * R * V_ * d_ * (prec_ == kF32 ? 3 : 1);
   } else if (kernel == 1) {  // log-softmax + top-k over R x V logits
     n_rows_.upload(&R, 1, stream_);
-    launch = [&] { launch_topk(logits_.get(), Vp_, beam_, stream_); };
-    *bytes = 4.0 * R * V_;
+    launch = [&] {
+      launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
+                          part_ld_, beam_, stream_);
+    };
+    *bytes = 12.0 * R * ((V_ + 31) / 32) + 4.0 * R * 32 * last_beam_;
     *flops = 0.0;
   } else if (kernel == 2) {  // decoder self-attention at the last step
     if (c.num_decoder_layers == 0) fail(kStateError, "no decoder layers");

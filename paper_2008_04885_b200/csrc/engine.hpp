@@ -83,6 +83,7 @@ class Engine {
   void stage(const std::vector<std::vector<int>>& srcs);
   void run_staged(const BeamConfigC& cfg);
   int64_t last_launches() const { return last_launches_; }
+  std::string diag_report() const;  // per-kernel step times (MTG_DIAG_EVENTS=1)
   cudaStream_t stream() const { return stream_; }
   // Times one hot kernel in isolation on the staged batch (see minimt_gpu.h).
   void time_kernel(int kernel, int iters, float* ms, double* bytes, double* flops);
@@ -100,11 +101,16 @@ class Engine {
   void gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
             long long ldc, const float* bias, const float* residual, int relu,
             long long c_step_stride = 0, const int* d_step = nullptr);
+  // Output projection into logits_ plus the per-slice softmax partials.
+  void gemm_logits(int m, const int* d_m);
   int stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status);
   void run_encoder(int n_sent, int m_enc, int max_src);
   void decoder_body();  // decoder layers + dec_final + logits for the live rows
   void decode_loop(int t_run);
-  void count() { ++launches_; }
+  // Launch accounting; with MTG_DIAG_EVENTS=1 the step graph also records an
+  // event after every kernel (breaks PDL overlap -- diagnostics only) and
+  // decode_loop accumulates per-kernel times for diag_report().
+  void count(const char* tag = "kernel");
 
   HostModel host_;
   int prec_;
@@ -112,6 +118,15 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   std::mutex mu_;
   int64_t launches_ = 0, last_launches_ = 0;
+  bool diag_ = false, capturing_ = false;
+  struct DiagMark {
+    std::string name;
+    cudaEvent_t ev;
+  };
+  std::vector<DiagMark> diag_marks_;
+  std::vector<double> diag_ms_;
+  int diag_steps_ = 0;
+  void diag_clear();
 
   // ---- weights ----
   DeviceBuffer<float> src_embed_, tgt_embed_f32_, pe_;
@@ -142,6 +157,9 @@ class Engine {
   DeviceBuffer<float> enc_x_, enc_a_, enc_qkv_, enc_ctx_, ffh_;
   std::vector<DeviceBuffer<float>> ckv_;
   DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;
+  DeviceBuffer<float> part_m_, part_s_;  // [r_max x part_ld_] softmax partials
+  DeviceBuffer<int> part_arg_;
+  long long part_ld_ = 0;
   std::vector<DeviceBuffer<float>> qkv_cache_;
   DeviceBuffer<int> src_ids_, src_pos_, src_off_, enc_off_, enc_len_, src_rowseg_;
   DeviceBuffer<float> rowmax_;  // per-row max |x| for int8 segment scales
@@ -149,7 +167,7 @@ class Engine {
   // beam state
   DeviceBuffer<int> step_, n_rows_, row_sent_, row_prev_, row_parent_, anc0_, anc1_, tok0_, tok1_,
       cand_tok_, sent_row0_, sent_live_, sent_maxlen_, sent_done_, best_has_, best_len_, best_tok_,
-      res_len_, res_status_, res_tok_, sel_parent_, sel_tok_;
+      res_len_, res_status_, res_tok_, sel_parent_, sel_tok_, sel_count_;
   DeviceBuffer<float> row_lp_, cand_score_, best_norm_, best_lp_, res_lp_, res_norm_, sel_lp_;
   DeviceBuffer<unsigned> res_flags_;
   BeamDev beam_{};

@@ -48,34 +48,46 @@ CUtensorMap make_map(const void* ptr, int prec, int rows, int k_pad, int box_row
   return m;
 }
 
-template <int PREC, int BN>
+template <int PREC, int BN, int EPI>
 void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN>,
+    MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN, EPI>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
   dim3 grid(p.n_tiles, p.m_tiles);
-  launch_k(gemm_tc_kernel<PREC, BN>, grid, kGemmThreads, p.smem, stream, p.a, p.b, p.a2, p.b2,
-                                                                   p.num_kb, p.nst, ep);
+  launch_k(gemm_tc_kernel<PREC, BN, EPI>, grid, kGemmThreads, p.smem, stream, p.a, p.b, p.a2,
+           p.b2, p.num_kb, p.nst, ep);
   MTG_CUDA(cudaGetLastError());
 }
 
 template <int PREC>
 void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  if (ep.part_m) {
+    if (ep.bias || ep.residual || ep.relu || ep.d_step)
+      fail(kStateError, "gemm: softmax-partials epilogue takes no bias/relu/residual");
+    if (ep.part_ld % 4 != 0 || ep.part_ld * 32 < ep.N)
+      fail(kStateError, "gemm: softmax partial pitch");
+    switch (p.bn) {
+      case 128: return launch_one<PREC, 128, kEpiSoftmaxParts>(p, ep, stream);
+      case 256: return launch_one<PREC, 256, kEpiSoftmaxParts>(p, ep, stream);
+    }
+    fail(kStateError, "gemm: softmax partials need a 128/256-column tile");
+  }
   switch (p.bn) {
-    case 32: return launch_one<PREC, 32>(p, ep, stream);
-    case 64: return launch_one<PREC, 64>(p, ep, stream);
-    case 128: return launch_one<PREC, 128>(p, ep, stream);
-    case 256: return launch_one<PREC, 256>(p, ep, stream);
+    case 32: return launch_one<PREC, 32, kEpiLinear>(p, ep, stream);
+    case 64: return launch_one<PREC, 64, kEpiLinear>(p, ep, stream);
+    case 128: return launch_one<PREC, 128, kEpiLinear>(p, ep, stream);
+    case 256: return launch_one<PREC, 256, kEpiLinear>(p, ep, stream);
   }
   fail(kStateError, "gemm: unsupported tile width");
 }
 
 }  // namespace
 
-GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn) {
+GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn,
+                   int min_bn) {
   if (a.prec != b.prec || a.k_pad != b.k_pad)
     fail(kShapeError, "gemm: operand precision / K mismatch");
   if (a.k_pad % (128 / prec_elem_bytes(a.prec)) != 0)
@@ -93,6 +105,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
         break;
       }
     }
+    bn = std::max(bn, min_bn);
   }
   p.bn = bn;
   p.n_tiles = (n + bn - 1) / bn;

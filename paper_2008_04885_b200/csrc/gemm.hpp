@@ -37,8 +37,10 @@ struct GemmPlan {
 };
 
 // Plans C[M x N] = A[M x K] . B[N x K]^T for at most m_max rows of A.
+// min_bn: smallest tile width the planner may pick (the softmax-partials
+// epilogue needs >= 128).
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n,
-                   int force_bn = 0);
+                   int force_bn = 0, int min_bn = 32);
 void launch_gemm(const GemmPlan& plan, const GemmEpilogue& ep, cudaStream_t stream);
 
 }  // namespace mtg

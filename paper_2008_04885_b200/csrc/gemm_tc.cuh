@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <cuda.h>
 
+#include "detmath.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
 
@@ -46,7 +47,18 @@ struct GemmEpilogue {
   int M;                     // rows, unless d_M != null
   const int* d_M;
   int N;
+  // Output-projection mode (EPI = 1, see kEpiSoftmaxParts): per 32-column
+  // slice of each row, its max, first argmax column and sum of exp(x - max).
+  float* part_m;             // [M x part_ld]
+  float* part_s;
+  int* part_arg;
+  long long part_ld;
 };
+
+// EPI = 0: linear-layer epilogue. EPI = 1: output projection; also emits the
+// log-softmax / top-k partials (no bias, relu or residual).
+constexpr int kEpiLinear = 0;
+constexpr int kEpiSoftmaxParts = 1;
 
 enum GemmPrec : int { kPrecI8 = 0, kPrecBF16 = 1, kPrecTF32x3 = 2 };
 
@@ -70,7 +82,7 @@ __host__ __device__ constexpr int gemm_tmem_cols(int bn) {
 constexpr int kGemmSmemExtra = 1024 /*align*/ + 256 /*barriers*/;
 constexpr int kEpiStageBytes = kEpiWarps * 32 * 33 * 4;  // aliases the drained pipeline
 
-template <int PREC, int BN>
+template <int PREC, int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB,
@@ -206,22 +218,31 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     }
     const long long step_off =
         ep.d_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride : 0LL;
+    const bool has_bias = ep.bias != nullptr, has_res = ep.residual != nullptr;
+    const bool relu = ep.relu != 0;
+    const int N = ep.N;
+    const long long ldc = ep.ldc, ldr = ep.ldr;
+    float* const Cbase = ep.C + step_off + static_cast<long long>(rbase) * ldc;
     // BN = 32 (the N = d_model residual GEMMs): each epilogue warp owns one
     // 32-row x 16-column chunk, so its residual and bias are fetched while
     // the MMAs are still running.
-    constexpr bool kPrefetch = (BN == 32);
+    constexpr bool kPrefetch = (BN == 32 && EPI == kEpiLinear);
     float res_pre[kPrefetch ? 32 : 1];
     float bias_pre = 0.0f;
     if constexpr (kPrefetch) {
       const int col = n0 + half * kHalf + (lane % kChunk);
-      const bool col_ok = col < ep.N && lane < kChunk;
+      const bool col_ok = col < N && lane < kChunk;
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        res_pre[i] = (ep.residual && col_ok && i < nrows)
-                         ? ep.residual[static_cast<long long>(rbase + i) * ep.ldr + col]
+        res_pre[i] = (has_res && col_ok && i < nrows)
+                         ? ep.residual[static_cast<long long>(rbase + i) * ldr + col]
                          : 0.0f;
-      if (ep.bias && col_ok) bias_pre = ep.bias[col];
+      if (has_bias && col_ok) bias_pre = ep.bias[col];
     }
+    // Softmax partials of this thread's row over its kHalf columns.
+    constexpr int kSubs = EPI == kEpiSoftmaxParts ? kHalf / 32 : 1;
+    float sub_m[kSubs], sub_s[kSubs];
+    int sub_a[kSubs];
     mbar_wait(accum_bar, 0);
     tc_fence_after();
 #pragma unroll 1
@@ -234,62 +255,143 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
                   *reinterpret_cast<uint32_t(*)[16]>(r));
       }
       tmem_ld_wait();
-      if (nrows <= 0 || n0 + c >= ep.N) continue;  // warp-uniform
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        float v;
-        if constexpr (PREC == kPrecI8) {
-          const int col = n0 + c + j;
-          const int seg = ep.seg_width > 0 ? min(col / ep.seg_width, kMaxSegments - 1) : 0;
+      if (nrows <= 0 || n0 + c >= N) continue;  // warp-uniform
+      float v[kChunk];
+      if constexpr (PREC == kPrecI8) {
+        if (ep.seg_width == 0 || ep.seg_width % kChunk == 0) {
+          // The weight segment is uniform over the chunk.
+          const int seg = ep.seg_width > 0 ? min((n0 + c) / ep.seg_width, kMaxSegments - 1) : 0;
           float iv = inv[0];
 #pragma unroll
           for (int s = 1; s < kMaxSegments; ++s) iv = seg == s ? inv[s] : iv;
-          v = __fmul_rn(__int2float_rn(static_cast<int>(r[j])), iv);
-        } else {
-          v = __uint_as_float(r[j]);
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j)
+            v[j] = __fmul_rn(__int2float_rn(static_cast<int>(r[j])), iv);
+        } else {  // narrow fused segments (tiny models): per column
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) {
+            const int seg = min((n0 + c + j) / ep.seg_width, kMaxSegments - 1);
+            float iv = inv[0];
+#pragma unroll
+            for (int s = 1; s < kMaxSegments; ++s) iv = seg == s ? inv[s] : iv;
+            v[j] = __fmul_rn(__int2float_rn(static_cast<int>(r[j])), iv);
+          }
         }
-        stage[lane * 33 + j] = v;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(r[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) stage[lane * 33 + j] = v[j];
+      if constexpr (EPI == kEpiSoftmaxParts) {
+        // Slice max / first argmax (strict >, so NaN never wins), then the
+        // sequential sum of exp(x - max) in column order (P6),
+        // re-reading the values from the staging tile (keeps the code small).
+        const int col0 = n0 + c;
+        const int nv = min(kChunk, N - col0);
+        float best = -__int_as_float(0x7f800000);
+        int bi = -1;
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const bool take = j < nv && v[j] > best;
+          best = take ? v[j] : best;
+          bi = take ? col0 + j : bi;
+        }
+        float sum = 0.0f;
+        if (bi >= 0) {
+          const float* sv = stage + lane * 33;
+#pragma unroll 4
+          for (int j = 0; j < nv; ++j) sum = __fadd_rn(sum, det_expf_nonpos(__fsub_rn(sv[j], best)));
+        }
+        const int k = (c - half * kHalf) / 32;
+#pragma unroll
+        for (int kk = 0; kk < kSubs; ++kk)
+          if (kk == k) {
+            sub_m[kk] = best;
+            sub_s[kk] = sum;
+            sub_a[kk] = bi;
+          }
       }
       __syncwarp();
       const int col = n0 + c + (lane % kChunk);
-      const bool col_ok = col < ep.N && lane < kChunk;
+      const bool col_ok = col < N && lane < kChunk;
+      float* cp = Cbase + col;
       if constexpr (kPrefetch) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          float v = stage[i * 33 + (lane % kChunk)];
-          if (ep.bias) v = __fadd_rn(v, bias_pre);
-          if (ep.relu) v = v > 0.0f ? v : 0.0f;
-          if (ep.residual) v = __fadd_rn(res_pre[i], v);
-          if (col_ok && i < nrows)
-            ep.C[step_off + static_cast<long long>(rbase + i) * ep.ldc + col] = v;
+          float x = stage[i * 33 + (lane % kChunk)];
+          if (has_bias) x = __fadd_rn(x, bias_pre);
+          if (relu) x = x > 0.0f ? x : 0.0f;
+          if (has_res) x = __fadd_rn(res_pre[i], x);
+          if (col_ok && i < nrows) cp[i * ldc] = x;
         }
         __syncwarp();
         continue;
       }
-      const float bias = (col_ok && ep.bias) ? ep.bias[col] : 0.0f;
+      if (EPI == kEpiSoftmaxParts || (!has_bias && !relu && !has_res)) {
+        if (col_ok) {
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i)
+            if (i < nrows) cp[i * ldc] = stage[i * 33 + lane];
+        }
+        __syncwarp();
+        continue;
+      }
+      const float bias = (col_ok && has_bias) ? ep.bias[col] : 0.0f;
+      const float* rp = has_res ? ep.residual + static_cast<long long>(rbase) * ldr + col : nullptr;
       // Residual loads of a row group are issued before its stores: C may
       // alias the residual, so loads placed after stores would serialise.
 #pragma unroll 1
       for (int i0 = 0; i0 < 32; i0 += 8) {
         float res[8];
-        if (ep.residual) {
+        if (has_res) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            res[i] = (col_ok && i0 + i < nrows)
-                         ? ep.residual[static_cast<long long>(rbase + i0 + i) * ep.ldr + col]
-                         : 0.0f;
+            res[i] = (col_ok && i0 + i < nrows) ? rp[(i0 + i) * ldr] : 0.0f;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          float v = stage[(i0 + i) * 33 + (lane % kChunk)];
-          if (ep.bias) v = __fadd_rn(v, bias);
-          if (ep.relu) v = v > 0.0f ? v : 0.0f;
-          if (ep.residual) v = __fadd_rn(res[i], v);
-          if (col_ok && i0 + i < nrows)
-            ep.C[step_off + static_cast<long long>(rbase + i0 + i) * ep.ldc + col] = v;
+          float x = stage[(i0 + i) * 33 + (lane % kChunk)];
+          if (has_bias) x = __fadd_rn(x, bias);
+          if (relu) x = x > 0.0f ? x : 0.0f;
+          if (has_res) x = __fadd_rn(res[i], x);
+          if (col_ok && i0 + i < nrows) cp[(i0 + i) * ldc] = x;
         }
       }
       __syncwarp();
+    }
+    if constexpr (EPI == kEpiSoftmaxParts) {
+      // Row rbase+lane, slices sub0 .. sub0+kSubs-1 (sub0 % kSubs == 0).
+      const int sub0 = (n0 + half * kHalf) / 32;
+      const int nsub = (N + 31) / 32;
+      if (lane < nrows && sub0 < nsub) {
+        const long long o = static_cast<long long>(rbase + lane) * ep.part_ld + sub0;
+        if (sub0 + kSubs <= nsub) {
+          if constexpr (kSubs == 4) {
+            *reinterpret_cast<float4*>(ep.part_m + o) =
+                make_float4(sub_m[0], sub_m[1], sub_m[2], sub_m[3]);
+            *reinterpret_cast<float4*>(ep.part_s + o) =
+                make_float4(sub_s[0], sub_s[1], sub_s[2], sub_s[3]);
+            *reinterpret_cast<int4*>(ep.part_arg + o) =
+                make_int4(sub_a[0], sub_a[1], sub_a[2], sub_a[3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < kSubs; ++k) {
+              ep.part_m[o + k] = sub_m[k];
+              ep.part_s[o + k] = sub_s[k];
+              ep.part_arg[o + k] = sub_a[k];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < kSubs; ++k)
+            if (sub0 + k < nsub) {
+              ep.part_m[o + k] = sub_m[k];
+              ep.part_s[o + k] = sub_s[k];
+              ep.part_arg[o + k] = sub_a[k];
+            }
+        }
+      }
     }
   }
 

@@ -111,6 +111,7 @@ struct BeamDev {
   int* sel_parent;    // [N * B]
   int* sel_tok;
   float* sel_lp;
+  int* sel_count;     // [1] CTAs of beam_select done this step (last one compacts)
   int N, B, T, R_max, V;
   float alpha;
   int max_seq_len;
@@ -120,11 +121,15 @@ struct BeamDev {
 void launch_beam_init(const BeamDev& b, cudaStream_t st);
 
 // log_softmax_row + candidate scores + per-row top-min(B,V) by (score desc,
-// token asc); one 1024-thread CTA per live row, logits held in registers
-// (topk.cu). The logits pitch must be topk_pitch(V) with the pad columns
-// set to -inf. Supports V <= 32768.
-long long topk_pitch(int V);
-void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st);
+// token asc), one warp per live row, from the per-32-column softmax partials
+// of the output-projection GEMM (gemm_tc.cuh kEpiSoftmaxParts) plus a
+// rescan of the few slices that can hold the winners (topk.cu). V <= 32768.
+constexpr int kMaxSoftmaxSlices = 1024;
+long long topk_pitch(int V);          // logits row pitch (elements)
+long long softmax_part_pitch(int V);  // partials row pitch (slices, multiple of 4)
+void launch_softmax_topk(const float* logits, long long ldl, const float* part_m,
+                         const float* part_s, const int* part_arg, long long part_ld,
+                         const BeamDev& b, cudaStream_t st);
 
 // Per-sentence selection of beam_size candidates by (score desc, parent asc,
 // token asc), EOS -> finished (running first-max of the GNMT score), live

@@ -1,17 +1,22 @@
 // log_softmax_row + candidate scores + per-row top-kB (decode.cpp:25-30,
-// 55-69), one 1024-thread CTA per live hypothesis row.
+// 55-69), from the partials the output-projection GEMM epilogue leaves behind
+// (gemm_tc.cuh, kEpiSoftmaxParts): for every 32-column slice k of a row, its
+// max m_k, first argmax column a_k and s_k = sum_j exp(x_j - m_k) in column
+// order. One 128-thread CTA per live hypothesis row:
 //
-// Thread t owns logits 4(t + 1024 i) + c, i < NV4, held in registers (one
-// HBM pass). The logits pitch is a multiple of 4096 and the pad columns hold
-// -inf (written once at allocation), so there are no bounds checks: a pad
-// element adds exp(-inf) = +0 to the sum and never scores. Sum order P2.
+//   M   = max_k m_k
+//   S   = sum over k of u_k,  u_k = s_k * exp(m_k - M)  (0 if m_k = -inf), in
+//         the P6 order: thread t of 128 sums k = t + 128 i in i order, P1
+//         butterfly per warp, then (W0 + W1) + (W2 + W3)
+//   lse = log(S) + M                                      (P6)
+//   score(x) = fl(parent_logprob + fl(x - lse))
 //
-// Top-kB by (score desc, token asc), score = fl(parent + fl(x - lse)), exact:
-// tau = kB-th largest per-warp max is <= the kB-th largest logit and score
-// is monotone in x, so every true top-kB element has score >= score(tau).
-// Those go to a shared list (normally ~kB entries) and warp 0 selects them
-// exactly; larger lists take block-wide rounds, and rows whose list
-// overflows (e.g. all-equal logits) take the exact slow path.
+// Top-kB by (score desc, token asc), exact: score is monotone in x, so an
+// element of slice k scores at most score(m_k). Let S_kB be the kB-th best
+// slice-max score (by the same order). Every element outside the slices with
+// score(m_k) >= S_kB scores < S_kB and ranks below kB slice maxima, so the
+// exact top-kB lies in those slices -- normally exactly kB of them -- which
+// are rescanned from the logits the GEMM wrote.
 #include <climits>
 
 #include "detmath.cuh"
@@ -24,7 +29,10 @@ namespace mtg {
 namespace {
 
 #define kNegInf (-__int_as_float(0x7f800000))
-constexpr int kListCap = 2048;
+#define kPosInf (__int_as_float(0x7f800000))
+constexpr int kMT = 128;                                 // threads per row (4 warps)
+constexpr int kSubPerThread = kMaxSoftmaxSlices / kMT;  // slices per thread (registers)
+constexpr int kCache = 4;                                // rescanned slices per warp in registers
 
 __device__ __forceinline__ bool better2(float a, int ta, float b, int tb) {
   return a > b || (a == b && ta < tb);
@@ -43,217 +51,197 @@ __device__ __forceinline__ void warp_best(float& bs, int& bt) {
   }
 }
 
-// Block-wide argmax over one candidate per thread; every thread gets it.
-__device__ __forceinline__ void block_best(float& bs, int& bt, float* red_f, int* red_i) {
+// CTA-wide (4 warps) argmax; every thread gets the winner.
+__device__ __forceinline__ void block_best(float& bs, int& bt, float* rf, int* ri) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   warp_best(bs, bt);
-  __syncthreads();
   if (lane == 0) {
-    red_f[warp] = bs;
-    red_i[warp] = bt;
+    rf[warp] = bs;
+    ri[warp] = bt;
   }
   __syncthreads();
-  bs = red_f[lane];
-  bt = red_i[lane];
-  warp_best(bs, bt);
+  bs = rf[0];
+  bt = ri[0];
+#pragma unroll
+  for (int w = 1; w < kMT / 32; ++w)
+    if (ri[w] != INT_MAX && (bt == INT_MAX || better2(rf[w], ri[w], bs, bt))) {
+      bs = rf[w];
+      bt = ri[w];
+    }
+  __syncthreads();
 }
 
-template <int NV4>
-__global__ void __launch_bounds__(kTopkThreads) topk_kernel(const float* __restrict__ logits,
-                                                            long long ldl, BeamDev b) {
+// One CTA (128 threads) per live hypothesis row; thread t owns slices
+// t + 128 i. Sum order P6: thread partials in i order, P1 butterfly per warp,
+// then (W0 + W1) + (W2 + W3).
+__global__ void __launch_bounds__(kMT)
+    softmax_topk_kernel(const float* __restrict__ logits, long long ldl,
+                        const float* __restrict__ part_m, const float* __restrict__ part_s,
+                        const int* __restrict__ part_arg, long long part_ld, int nsub,
+                        BeamDev b) {
   pdl_wait();
   pdl_trigger();
+  __shared__ float red_f[kMT / 32];
+  __shared__ int red_i[kMT / 32];
+  __shared__ int list_s[kMaxSoftmaxSlices];
+  __shared__ int n_list_s;
   const int r = blockIdx.x;
-  if (r >= *b.n_rows) return;
-  __shared__ float red_f[32];
-  __shared__ int red_i[32];
-  __shared__ float list_s[kListCap];
-  __shared__ int list_t[kListCap];
-  __shared__ int list_n;
+  if (r >= *b.n_rows) return;  // uniform over the CTA
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = b.V;
-  const float* x = logits + r * ldl;
-  if (tid == 0) list_n = 0;
-
-  float v[NV4 * 4];
-#pragma unroll
-  for (int i = 0; i < NV4; ++i) {
-    const float4 f = *reinterpret_cast<const float4*>(x + 4 * (tid + kTopkThreads * i));
-    v[4 * i] = f.x;
-    v[4 * i + 1] = f.y;
-    v[4 * i + 2] = f.z;
-    v[4 * i + 3] = f.w;
-  }
-  float tmax = kNegInf;
-#pragma unroll
-  for (int i = 0; i < NV4 * 4; ++i) tmax = fmaxf(tmax, v[i]);
-  const float wmax = warp_allmax(tmax);
-  if (lane == 0) red_f[warp] = wmax;
-  __syncthreads();
-  const float wm = red_f[lane];  // lane l holds warp l's max
-  const float mx = warp_allmax(wm);
   const int kB = min(b.B, V);
-  // tau = kB-th largest warp max: kB warps each hold an element >= tau, so
-  // tau <= the kB-th largest logit. Every warp computes it (shuffles only).
-  float tau = kNegInf;
-  {
-    float c = wm;
-    int ct = wm == kNegInf ? INT_MAX : lane;
-    for (int k = 0; k < kB; ++k) {
-      float bs = c;
-      int bt = ct;
-      warp_best(bs, bt);
-      if (bt == INT_MAX) {
-        tau = kNegInf;
-        break;
-      }
-      tau = bs;
-      if (bt == lane) {
-        c = kNegInf;
-        ct = INT_MAX;
-      }
-    }
-  }
-  __syncthreads();
+  const float* pm = part_m + r * part_ld;
+  const float* ps = part_s + r * part_ld;
+  const int* pa = part_arg + r * part_ld;
+  const float* x = logits + r * ldl;
+  const float plp = b.row_lp[r];
+  if (tid == 0) n_list_s = 0;
 
+  // All partial loads first (one L2 round trip), then the math.
+  float mv[kSubPerThread], sv[kSubPerThread];
+  int at[kSubPerThread];
+#pragma unroll
+  for (int i = 0; i < kSubPerThread; ++i) {
+    const int k = tid + kMT * i;
+    const bool ok = k < nsub;
+    mv[i] = ok ? pm[k] : kNegInf;
+    sv[i] = ok ? ps[k] : 0.0f;
+    at[i] = ok ? pa[k] : -1;
+  }
+  float mloc = kNegInf;
+#pragma unroll
+  for (int i = 0; i < kSubPerThread; ++i) mloc = fmaxf(mloc, mv[i]);
+  mloc = warp_allmax(mloc);
+  if (lane == 0) red_f[warp] = mloc;
+  __syncthreads();
+  const float M = fmaxf(fmaxf(red_f[0], red_f[1]), fmaxf(red_f[2], red_f[3]));
+  __syncthreads();
   float part = 0.0f;
 #pragma unroll
-  for (int i = 0; i < NV4 * 4; ++i) part = __fadd_rn(part, det_expf_nonpos(__fsub_rn(v[i], mx)));
+  for (int i = 0; i < kSubPerThread; ++i) {
+    if (tid + kMT * i < nsub) {
+      const float u =
+          mv[i] == kNegInf ? 0.0f : __fmul_rn(sv[i], det_expf_nonpos(__fsub_rn(mv[i], M)));
+      part = __fadd_rn(part, u);
+    }
+  }
   part = warp_allsum(part);
   if (lane == 0) red_f[warp] = part;
   __syncthreads();
-  const float total = warp_allsum(red_f[lane]);
-  const float lse = __fadd_rn(det_logf(total), mx);
-  const float plp = b.row_lp[r];
-
-  // Candidates: score >= score(tau). Branch-free mask first; the few threads
-  // holding candidates append them (one shared atomic per thread).
-  const float s_lb = tau == kNegInf ? kNegInf : __fadd_rn(plp, __fsub_rn(tau, lse));
-  unsigned mask = 0u;
-#pragma unroll
-  for (int i = 0; i < NV4 * 4; ++i) {
-    const float sc = __fadd_rn(plp, __fsub_rn(v[i], lse));
-    mask |= (sc >= s_lb && v[i] != kNegInf) ? (1u << i) : 0u;  // -inf: pad column
-  }
-  if (mask) {
-    int slot = atomicAdd(&list_n, __popc(mask));
-#pragma unroll
-    for (int i = 0; i < NV4 * 4; ++i)
-      if ((mask >> i) & 1u) {
-        if (slot < kListCap) {
-          list_s[slot] = __fadd_rn(plp, __fsub_rn(v[i], lse));
-          list_t[slot] = 4 * (tid + kTopkThreads * (i >> 2)) + (i & 3);
-        }
-        ++slot;
-      }
-  }
+  const float total = __fadd_rn(__fadd_rn(red_f[0], red_f[1]), __fadd_rn(red_f[2], red_f[3]));
   __syncthreads();
-  const int n_list = list_n;
+  const float lse = __fadd_rn(det_logf(total), M);
 
-  if (n_list <= 64) {  // common case: warp 0 alone, shuffles only
-    if (warp != 0) return;
-    unsigned taken = 0u;
-    for (int k = 0; k < kB; ++k) {
-      float bs = kNegInf;
-      int bt = INT_MAX, be = -1;
+  // Slice-max scores; a slice with no max (all NaN / empty) never competes.
+  float sc[kSubPerThread];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int idx = lane + 32 * e;
-        if (idx < n_list && !((taken >> e) & 1u) &&
-            (bt == INT_MAX || better2(list_s[idx], list_t[idx], bs, bt))) {
-          bs = list_s[idx];
-          bt = list_t[idx];
-          be = e;
-        }
-      }
-      float ws = bs;
-      int wt = bt;
-      warp_best(ws, wt);
-      if (lane == 0) {
-        b.cand_score[static_cast<long long>(r) * b.B + k] = ws;
-        b.cand_tok[static_cast<long long>(r) * b.B + k] = wt;
-      }
-      if (bt == wt && be >= 0) taken |= 1u << be;
-    }
-    return;
+  for (int i = 0; i < kSubPerThread; ++i) {
+    sc[i] = __fadd_rn(plp, __fsub_rn(mv[i], lse));
+    if (sc[i] != sc[i]) at[i] = -1;
   }
-
-  if (n_list <= kListCap) {  // block-wide rounds over the list
-    unsigned taken = 0u;
-    for (int k = 0; k < kB; ++k) {
-      float bs = kNegInf;
-      int bt = INT_MAX;
-#pragma unroll
-      for (int e = 0; e < kListCap / kTopkThreads; ++e) {
-        const int idx = tid + kTopkThreads * e;
-        if (idx < n_list && !((taken >> e) & 1u) &&
-            (bt == INT_MAX || better2(list_s[idx], list_t[idx], bs, bt))) {
-          bs = list_s[idx];
-          bt = list_t[idx];
-        }
-      }
-      block_best(bs, bt, red_f, red_i);
-      if (tid == 0) {
-        b.cand_score[static_cast<long long>(r) * b.B + k] = bs;
-        b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
-      }
-#pragma unroll
-      for (int e = 0; e < kListCap / kTopkThreads; ++e) {
-        const int idx = tid + kTopkThreads * e;
-        if (idx < n_list && list_t[idx] == bt) taken |= 1u << e;
-      }
-    }
-    return;
-  }
-
-  // Slow exact path: kB block rounds over every element with a taken mask.
-  unsigned long long taken = 0ull;
+  // kB-th best slice max: kB rounds, each taking the best entry ranked
+  // strictly below the previous pick.
+  float last_s = kPosInf, thr = kNegInf;
+  int last_t = -1;
   for (int k = 0; k < kB; ++k) {
     float bs = kNegInf;
     int bt = INT_MAX;
 #pragma unroll
-    for (int i = 0; i < NV4 * 4; ++i) {
-      const int j = 4 * (tid + kTopkThreads * (i >> 2)) + (i & 3);
-      if (j < V && !((taken >> i) & 1ull)) {
-        const float sc = __fadd_rn(plp, __fsub_rn(v[i], lse));
-        if (bt == INT_MAX || better2(sc, j, bs, bt)) {
-          bs = sc;
-          bt = j;
+    for (int i = 0; i < kSubPerThread; ++i)
+      if (at[i] >= 0 && better2(last_s, last_t, sc[i], at[i]) &&
+          (bt == INT_MAX || better2(sc[i], at[i], bs, bt))) {
+        bs = sc[i];
+        bt = at[i];
+      }
+    block_best(bs, bt, red_f, red_i);
+    if (bt == INT_MAX) {  // fewer than kB slices: every valid slice is rescanned
+      thr = kNegInf;
+      break;
+    }
+    last_s = bs;
+    last_t = bt;
+    thr = bs;
+  }
+  // Slices to rescan: score(m_k) >= thr (normally exactly kB of them).
+#pragma unroll
+  for (int i = 0; i < kSubPerThread; ++i)
+    if (at[i] >= 0 && sc[i] >= thr) list_s[atomicAdd(&n_list_s, 1)] = tid + kMT * i;
+  __syncthreads();
+  const int n_list = n_list_s;
+  // Exact top-kB over the rescanned slices: warp w takes list entries
+  // w, w + 4, ...; lane = column within the slice.
+  constexpr int kW = kMT / 32;
+  float cs[kCache];
+  int cc[kCache];
+#pragma unroll
+  for (int e = 0; e < kCache; ++e) {  // loads issued back to back (clamped address)
+    const int idx = warp + kW * e;
+    cc[e] = idx < n_list ? list_s[idx] * 32 + lane : V;
+    cs[e] = x[min(cc[e], V - 1)];
+  }
+#pragma unroll
+  for (int e = 0; e < kCache; ++e)
+    cs[e] = cc[e] < V ? __fadd_rn(plp, __fsub_rn(cs[e], lse)) : kNegInf;
+  last_s = kPosInf;
+  last_t = -1;
+  for (int k = 0; k < kB; ++k) {
+    float bs = kNegInf;
+    int bt = INT_MAX;
+#pragma unroll
+    for (int e = 0; e < kCache; ++e) {
+      const int col = cc[e];
+      if (col < V && cs[e] == cs[e] && better2(last_s, last_t, cs[e], col) &&
+          (bt == INT_MAX || better2(cs[e], col, bs, bt))) {
+        bs = cs[e];
+        bt = col;
+      }
+    }
+    for (int idx = warp + kW * kCache; idx < n_list; idx += kW) {  // long lists (ties)
+      const int col = list_s[idx] * 32 + lane;
+      if (col < V) {
+        const float s = __fadd_rn(plp, __fsub_rn(x[col], lse));
+        if (s == s && better2(last_s, last_t, s, col) && (bt == INT_MAX || better2(s, col, bs, bt))) {
+          bs = s;
+          bt = col;
         }
       }
     }
     block_best(bs, bt, red_f, red_i);
     if (tid == 0) {
-      b.cand_score[static_cast<long long>(r) * b.B + k] = bs;
+      b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
       b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
     }
-    if (((bt >> 2) % kTopkThreads) == tid)
-      taken |= 1ull << (4 * ((bt >> 2) / kTopkThreads) + (bt & 3));
+    if (bt == INT_MAX) break;
+    last_s = bs;
+    last_t = bt;
+  }
+  // Rows with fewer than kB candidates leave the rest invalid.
+  for (int k = kB + tid; k < b.B; k += kMT) {
+    b.cand_score[static_cast<long long>(r) * b.B + k] = kNegInf;
+    b.cand_tok[static_cast<long long>(r) * b.B + k] = INT_MAX;
   }
 }
 
 }  // namespace
 
 long long topk_pitch(int V) {
-  const long long per = 4LL * kTopkThreads;
+  const long long per = 128;
   return (static_cast<long long>(V) + per - 1) / per * per;
 }
 
-void launch_topk(const float* logits, long long ldl, const BeamDev& b, cudaStream_t st) {
-  const int nv4 = static_cast<int>(topk_pitch(b.V) / (4 * kTopkThreads));
-  if (ldl < topk_pitch(b.V)) fail(kStateError, "topk: logits pitch must be topk_pitch(V)");
+long long softmax_part_pitch(int V) { return ((V + 31) / 32 + 3) / 4 * 4; }
+
+void launch_softmax_topk(const float* logits, long long ldl, const float* part_m,
+                         const float* part_s, const int* part_arg, long long part_ld,
+                         const BeamDev& b, cudaStream_t st) {
   if (b.B > kMaxBeam) fail(kUsageError, "beam size above 16 is not supported");
-  const dim3 grid(b.R_max), block(kTopkThreads);
-  if (nv4 <= 1)
-    launch_k(topk_kernel<1>, grid, block, 0, st, logits, ldl, b);
-  else if (nv4 <= 2)
-    launch_k(topk_kernel<2>, grid, block, 0, st, logits, ldl, b);
-  else if (nv4 <= 4)
-    launch_k(topk_kernel<4>, grid, block, 0, st, logits, ldl, b);
-  else if (nv4 <= 8)
-    launch_k(topk_kernel<8>, grid, block, 0, st, logits, ldl, b);
-  else
+  const int nsub = (b.V + 31) / 32;
+  if (nsub > kMaxSoftmaxSlices)
     fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
+  if (part_ld < nsub || ldl < b.V) fail(kStateError, "softmax_topk: pitches");
+  const dim3 grid(b.R_max), block(kMT);
+  launch_k(softmax_topk_kernel, grid, block, 0, st, logits, ldl, part_m, part_s, part_arg, part_ld,
+           nsub, b);
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -1,0 +1,12 @@
+# Per-kernel decode-step times: events after every kernel in the step graph
+# (serialised -- no PDL overlap), averaged over the steps of one batch.
+import os, sys
+os.environ["MTG_DIAG_EVENTS"] = "1"
+sys.path.insert(0, '/root/repo')
+import paper_2008_04885_b200 as mt
+from bench import CONFIG_20_2, sources
+prec = {'f32': mt.F32, 'int8': mt.INT8, 'bf16': mt.BF16}[sys.argv[1] if len(sys.argv) > 1 else 'int8']
+m = mt.Model.create(CONFIG_20_2, seed=1, precision=prec)
+m.stage(sources(64, 7)); cfg = mt.BeamConfig(5, 0, 1.0)
+m.run_staged(cfg); m.run_staged(cfg)
+print(m.diag_report())

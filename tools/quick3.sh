@@ -1,0 +1,8 @@
+set -x
+python -m pytest tests -m gpu -q -x 2>&1 | tail -5
+python bench.py --steps 5 --warmup 3 --precision int8 --no-cpu-baseline > gpurun_out/q_bench_int8.json 2> gpurun_out/q_bench_int8.err
+python -c "import json; d=json.load(open('gpurun_out/q_bench_int8.json')); print(d['value'], d['ms_per_step'], d['kernels'])"
+python tools/profile_step.py int8 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --profile-from-start off --csv --log-file gpurun_out/q_launches_int8_warm.csv python tools/profile_step.py int8 > gpurun_out/q_ncu.log 2>&1
+python tools/launches.py gpurun_out/q_launches_int8_warm.csv > gpurun_out/q_launches.txt; head -14 gpurun_out/q_launches.txt
+ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:softmax_topk -s 20 -c 1 -o gpurun_out/r01_softmax_topk_int8 python tools/profile_step.py int8 > gpurun_out/ncu_d.log 2>&1
+ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:beam_select -s 20 -c 1 -o gpurun_out/r01_beam_select_int8 python tools/profile_step.py int8 > gpurun_out/ncu_e.log 2>&1
