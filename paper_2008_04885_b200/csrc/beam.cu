@@ -309,6 +309,7 @@ __global__ void beam_reorder_kernel(BeamDev b) {
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;
   const int tn = *b.step;
+  if (tn < 1) return;
   const int cur = (tn - 1) & 1, nxt = tn & 1;
   const int T = b.T;
   const int pr = b.row_parent[r];

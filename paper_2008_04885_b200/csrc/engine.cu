@@ -200,6 +200,14 @@ void Engine::upload_weights() {
     tgt_embed_q_.resize(te.q.size());
     tgt_embed_q_.upload(te.q.data(), te.q.size(), stream_);
     tgt_scale_ = te.scale;
+    // The int8 embedding lookup is q / scale (quant.cpp dequantize); the
+    // table is dequantized once here (IEEE division, same bits as on device)
+    // so the per-step lookup is a plain fp32 row read.
+    std::vector<float> deq(te.q.size());
+    for (size_t i = 0; i < deq.size(); ++i) deq[i] = static_cast<float>(te.q[i]) / te.scale;
+    tgt_embed_f32_.resize(deq.size());
+    tgt_embed_f32_.upload(deq.data(), deq.size(), stream_);
+    MTG_CUDA(cudaStreamSynchronize(stream_));
   } else {
     upload_vec(tgt_embed_f32_, te);
   }
@@ -600,29 +608,72 @@ void Engine::run_encoder(int n_sent, int m, int max_src) {
     gemm(act_d_, dec_[l].cross_kv, m, nullptr, ckv_[l].get(), 2 * d, nullptr, nullptr, 0);
 }
 
-void Engine::decoder_body() {
+void Engine::decoder_body(bool reorder) {
   const ModelConfig& c = host_.config;
   const long long d = d_;
   const int R = r_max_;
   const int* dr = n_rows_.get();
   const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
   const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
-  launch_embed_tgt(row_prev_.get(), dr, R, step_.get(), tgt_embed_f32_.get(),
-                   prec_ == kINT8 ? tgt_embed_q_.get() : nullptr, tgt_scale_, d_, sqrt_d,
-                   pe_.get(), dec_y_.get(), d, stream_);
-  count("embed_tgt");
   // Decoder rows are their own quantization segments (one hypothesis row per
   // Executor::linear call in decode_step), so LayerNorm and attention write
   // the next GEMM's operand directly.
   const OperandOut od = opout(act_d_);
   auto ln_dec = [&](const LN& ln) {
-    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), dec_a_.get(), d, nullptr,
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), nullptr, d, nullptr,
                      &od, stream_);
     count("layernorm");
   };
+  // Step start: history reorder + target embedding + first LayerNorm fused
+  // into one kernel (d_model <= 512), else three kernels.
+  // MTG_STEP_FUSION: 0 = three kernels, 1 = reorder + fused embed/LN,
+  // 2 = one kernel (A/B switch; default 0: measured fastest with PDL).
+  static const int fusion = [] {
+    const char* e = std::getenv("MTG_STEP_FUSION");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool fused = d_ <= 512 && fusion > 0;
+  const LN& ln0 = c.num_decoder_layers > 0 ? dec_[0].n1 : dec_final_;
+  if (fused) {
+    StepBegin sb{};
+    sb.d_rows = dr;
+    sb.d_step = step_.get();
+    sb.prev = row_prev_.get();
+    sb.table = tgt_embed_f32_.get();
+    sb.table_q = nullptr;  // int8: tgt_embed_f32_ holds q / scale
+    sb.q_scale = tgt_scale_;
+    sb.sqrt_d = sqrt_d;
+    sb.pe = pe_.get();
+    sb.d = d_;
+    sb.x = dec_y_.get();
+    sb.ldx = d;
+    sb.reorder = reorder && fusion == 2 ? 1 : 0;
+    if (reorder && fusion != 2) {
+      launch_beam_reorder(beam_, stream_);
+      count("beam reorder");
+    }
+    sb.row_parent = row_parent_.get();
+    sb.anc[0] = anc0_.get();
+    sb.anc[1] = anc1_.get();
+    sb.tok[0] = tok0_.get();
+    sb.tok[1] = tok1_.get();
+    sb.T = T_;
+    launch_step_begin(sb, R, ln0.g.get(), ln0.b.get(), od, stream_);
+    count(sb.reorder ? "step begin (reorder+embed+LN)" : "step begin (embed+LN)");
+  } else {
+    if (reorder) {
+      launch_beam_reorder(beam_, stream_);
+      count("beam reorder");
+    }
+    launch_embed_tgt(row_prev_.get(), dr, R, step_.get(), tgt_embed_f32_.get(), nullptr,
+                     tgt_scale_, d_, sqrt_d,
+                     pe_.get(), dec_y_.get(), d, stream_);
+    count("embed_tgt");
+    ln_dec(ln0);
+  }
   for (int l = 0; l < c.num_decoder_layers; ++l) {
     DecLayer& L = dec_[l];
-    ln_dec(L.n1);
+    if (l > 0) ln_dec(L.n1);
     gemm(act_d_, L.self_qkv, R, dr, qkv_cache_[l].get(), 3 * d, nullptr, nullptr, 0,
          static_cast<long long>(R) * 3 * d, step_.get());
     launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
@@ -641,7 +692,7 @@ void Engine::decoder_body() {
     prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
     gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
   }
-  ln_dec(dec_final_);
+  if (c.num_decoder_layers > 0) ln_dec(dec_final_);
   gemm_logits(R, dr);
 }
 
@@ -667,14 +718,12 @@ void Engine::ensure_step_graph() {
       MTG_CUDA(cudaEventCreate(&diag_marks_.back().ev));
       MTG_CUDA(cudaEventRecordWithFlags(diag_marks_.back().ev, stream_, cudaEventRecordExternal));
     }
-    decoder_body();
+    decoder_body(true);
     launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
                         part_ld_, beam_, stream_);
     count("softmax + top-k merge");
     launch_beam_select(beam_, stream_);
     count("beam select");
-    launch_beam_reorder(beam_, stream_);
-    count("beam reorder");
   } catch (...) {
     capturing_ = false;
     cudaGraph_t g = nullptr;
@@ -896,7 +945,7 @@ void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int*
   std::vector<float> rows(size_t(n) * Vp_);
   std::vector<int> prev(n);
   for (int t = 0; t < nf; ++t) {
-    decoder_body();
+    decoder_body(false);
     MTG_CUDA(cudaStreamSynchronize(stream_));
     logits_.download(rows.data(), rows.size(), stream_);
     for (int s = 0; s < n; ++s)

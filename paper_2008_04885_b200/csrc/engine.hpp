@@ -105,7 +105,8 @@ class Engine {
   void gemm_logits(int m, const int* d_m);
   int stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status);
   void run_encoder(int n_sent, int m_enc, int max_src);
-  void decoder_body();  // decoder layers + dec_final + logits for the live rows
+  // reorder: beam search (copy histories from row_parent at step >= 1).
+  void decoder_body(bool reorder);  // decoder layers + dec_final + logits for the live rows
   void decode_loop(int t_run);
   // Launch accounting; with MTG_DIAG_EVENTS=1 the step graph also records an
   // event after every kernel (breaks PDL overlap -- diagnostics only) and

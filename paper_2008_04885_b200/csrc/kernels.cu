@@ -3,6 +3,9 @@
 // xor butterfly, P2 512-thread block sums, P3 sequential dot products,
 // context sums in key order, Cephes exp/log (detmath.cuh).
 #include <climits>
+#include <map>
+#include <mutex>
+#include <string>
 
 #include "detmath.cuh"
 #include "errors.hpp"
@@ -89,27 +92,15 @@ __global__ void embed_tgt_kernel(const int* __restrict__ prev, const int* d_rows
 
 // Row value c = lane + 32 i kept in registers (n <= 32*KPL): one pass over
 // HBM, no reload-after-store. Same P1 order as the generic kernel.
+// LayerNorm of one row held in registers (value c = lane + 32 i, n <= 32*KPL)
+// by one warp; writes y (optional), rowmax (optional) and the next GEMM's
+// operand (optional). P1 sums.
 template <int KPL>
-__global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx, int max_rows,
-                                     const int* d_rows, int n, const float* __restrict__ g,
-                                     const float* __restrict__ b, float* __restrict__ y,
-                                     long long ldy, float* __restrict__ rowmax, OperandOut op,
-                                     int has_op) {
-  pdl_wait();
-  pdl_trigger();
-  const int rows = d_rows ? *d_rows : max_rows;
-  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float* xr = x + r * ldx;
-  float xv[KPL], gv[KPL], bv[KPL];  // gain/bias loaded up front with x
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const int c = lane + 32 * i;
-    xv[i] = c < n ? xr[c] : 0.0f;
-    gv[i] = c < n ? g[c] : 0.0f;
-    bv[i] = c < n ? b[c] : 0.0f;
-  }
+__device__ __forceinline__ void ln_row_regs(float (&xv)[KPL], const float (&gv)[KPL],
+                                            const float (&bv)[KPL], int n, int lane, long long r,
+                                            float* __restrict__ y, long long ldy,
+                                            float* __restrict__ rowmax, const OperandOut& op,
+                                            int has_op) {
   float part = 0.0f;
 #pragma unroll
   for (int i = 0; i < KPL; ++i)
@@ -148,7 +139,7 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
   if (op.prec == 0) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(op.nonfinite, 1);
     const float scale = qscale_of(mx);
-    int8_t* q = op.q + static_cast<long long>(r) * op.k_pad;
+    int8_t* q = op.q + r * op.k_pad;
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const int c = lane + 32 * i;
@@ -157,7 +148,7 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
     for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) q[c] = 0;
     if (lane == 0) op.row_scale[r] = scale;
   } else if (op.prec == 1) {
-    __nv_bfloat16* h = op.h + static_cast<long long>(r) * op.k_pad;
+    __nv_bfloat16* h = op.h + r * op.k_pad;
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const int c = lane + 32 * i;
@@ -165,8 +156,8 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
     }
     for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) h[c] = __float2bfloat16_rn(0.0f);
   } else {
-    float* hi = op.hi + static_cast<long long>(r) * op.k_pad;
-    float* lo = op.lo + static_cast<long long>(r) * op.k_pad;
+    float* hi = op.hi + r * op.k_pad;
+    float* lo = op.lo + r * op.k_pad;
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const int c = lane + 32 * i;
@@ -183,6 +174,100 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
       lo[c] = 0.0f;
     }
   }
+}
+
+// Row value c = lane + 32 i kept in registers (n <= 32*KPL): one pass over
+// HBM, no reload-after-store. Same P1 order as the generic kernel.
+template <int KPL>
+__global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx, int max_rows,
+                                     const int* d_rows, int n, const float* __restrict__ g,
+                                     const float* __restrict__ b, float* __restrict__ y,
+                                     long long ldy, float* __restrict__ rowmax, OperandOut op,
+                                     int has_op) {
+  pdl_wait();
+  pdl_trigger();
+  const int rows = d_rows ? *d_rows : max_rows;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + r * ldx;
+  float xv[KPL], gv[KPL], bv[KPL];  // gain/bias loaded up front with x
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    xv[i] = c < n ? xr[c] : 0.0f;
+    gv[i] = c < n ? g[c] : 0.0f;
+    bv[i] = c < n ? b[c] : 0.0f;
+  }
+  ln_row_regs<KPL>(xv, gv, bv, n, lane, r, y, ldy, rowmax, op, has_op);
+}
+
+// First kernel of a decode step, one warp per live row r:
+//  * (reorder) copy the parent's ancestor / token history into row r
+//    (decode.cpp:82-86 hypothesis copy) when step >= 1 and reorder != 0;
+//  * target embedding of the previous token + positional encoding
+//    (model.cpp:600-612), written to the residual stream x;
+//  * the first decoder LayerNorm, written as the next GEMM's operand.
+template <int KPL>
+__global__ void step_begin_kernel(StepBegin sb, const float* __restrict__ g,
+                                  const float* __restrict__ bln, OperandOut op) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= *sb.d_rows) return;
+  const int t = *sb.d_step;
+  const int n = sb.d;
+  const long long id = sb.prev[r];
+  const bool reo = sb.reorder && t >= 1;
+  const int pr = reo ? sb.row_parent[r] : 0;
+  float xv[KPL], gv[KPL], bv[KPL];
+  const float* pe = sb.pe + static_cast<long long>(t) * n;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    float e = 0.0f;
+    if (c < n)
+      e = sb.table_q ? __fdiv_rn(static_cast<float>(sb.table_q[id * n + c]), sb.q_scale)
+                     : sb.table[id * n + c];
+    xv[i] = c < n ? __fadd_rn(__fmul_rn(e, sb.sqrt_d), pe[c]) : 0.0f;
+    gv[i] = c < n ? g[c] : 0.0f;
+    bv[i] = c < n ? bln[c] : 0.0f;
+  }
+  if (reo) {  // all history loads first, then the stores
+    const int T = sb.T;
+    const int cur = (t - 1) & 1, nxt = t & 1;
+    const int* ac = sb.anc[cur] + static_cast<long long>(pr) * T;
+    int* an = sb.anc[nxt] + static_cast<long long>(r) * T;
+    const int* tc = sb.tok[cur] + static_cast<long long>(pr) * T;
+    int* tn = sb.tok[nxt] + static_cast<long long>(r) * T;
+    const int na = min(t, T), nt = t - 1;
+    constexpr int kH = 4;
+    int av[kH], tv[kH];
+#pragma unroll
+    for (int k = 0; k < kH; ++k) {
+      const int j = lane + 32 * k;
+      av[k] = j < na ? ac[j] : 0;
+      tv[k] = j < nt ? tc[j] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kH; ++k) {
+      const int j = lane + 32 * k;
+      if (j < na) an[j] = av[k];
+      if (j < nt) tn[j] = tv[k];
+    }
+    for (int j = 32 * kH + lane; j < na; j += 32) an[j] = ac[j];
+    for (int j = 32 * kH + lane; j < nt; j += 32) tn[j] = tc[j];
+    if (lane == 0) {
+      if (t < T) an[t] = r;
+      if (t - 1 < T) tn[t - 1] = static_cast<int>(id);
+    }
+  }
+  float* xr = sb.x + r * sb.ldx;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i)
+    if (lane + 32 * i < n) xr[lane + 32 * i] = xv[i];
+  ln_row_regs<KPL>(xv, gv, bv, n, lane, r, nullptr, 0, nullptr, op, 1);
 }
 
 __global__ void layernorm_kernel(const float* __restrict__ x, long long ldx, int max_rows,
@@ -457,6 +542,124 @@ __device__ __forceinline__ void finish_ctx_row(const float* row, int d, long lon
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) & ~3; }
 
+// ---- staged decoder attention (head dim 64) ----------------------------------
+// Key and value rows are copied global -> shared with cp.async, a whole row
+// per half-warp (coalesced), into a per-warp stage with an XOR swizzle of the
+// 16-byte columns, so the lane-per-key reads that follow are conflict-free.
+// Same arithmetic (P3 dots, P1 softmax, P1 context) as attend_warp<64>.
+constexpr int kStageFloats = 32 * 64;  // one 32-key chunk of 64-float rows
+
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_warp() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
+// Rows c0 .. c0+31 (< n) as [32][64]; float4 column c of row jr at c ^ (jr & 15).
+template <class KP>
+__device__ __forceinline__ void stage_rows64(float* stage, int c0, int n, KP kp, int lane) {
+  const int c = lane & 15, half = lane >> 4;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int jr = 2 * i + half, j = c0 + jr;
+    if (j < n) cp_async16(stage + jr * 64 + ((c ^ (jr & 15)) << 2), kp(j) + 4 * c);
+  }
+  cp_async_commit();
+}
+
+// Columns col0 .. col0+31 of rows c0 .. c0+31 as [32][32]; float4 column c of
+// row jr at c ^ (jr & 7).
+template <class VP>
+__device__ __forceinline__ void stage_half32(float* stage, int c0, int n, int col0, VP vp,
+                                             int lane) {
+  const int c = lane & 7, q4 = lane >> 3;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int jr = 4 * i + q4, j = c0 + jr;
+    if (j < n) cp_async16(stage + jr * 32 + ((c ^ (jr & 7)) << 2), vp(j) + col0 + 4 * c);
+  }
+  cp_async_commit();
+}
+
+template <class KP, class VP>
+__device__ __forceinline__ void attend_warp_staged64(const float* q, int n, float scale, KP kp,
+                                                     VP vp, float* stage, float* s, float* out) {
+  const int lane = threadIdx.x & 31;
+  float mx = kNegInf;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    stage_rows64(stage, c0, n, kp, lane);
+    cp_async_wait_warp();
+    const int j = c0 + lane;
+    if (j < n) {
+      const float* kr = stage + lane * 64;
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float4 kv = lds_f4(kr + ((c ^ (lane & 15)) << 2));
+        const float4 qv = lds_f4(q + 4 * c);
+        acc = __fadd_rn(acc, __fmul_rn(qv.x, kv.x));
+        acc = __fadd_rn(acc, __fmul_rn(qv.y, kv.y));
+        acc = __fadd_rn(acc, __fmul_rn(qv.z, kv.z));
+        acc = __fadd_rn(acc, __fmul_rn(qv.w, kv.w));
+      }
+      const float v = __fmul_rn(acc, scale);
+      s[j] = v;
+      mx = fmaxf(mx, v);
+    }
+    __syncwarp();
+  }
+  stage_half32(stage, 0, n, 0, vp, lane);  // first value chunk overlaps the softmax
+  mx = warp_allmax(mx);
+  float part = 0.0f;
+  for (int j = lane; j < n; j += 32) {
+    const float e = det_expf_nonpos(__fsub_rn(s[j], mx));
+    s[j] = e;
+    part = __fadd_rn(part, e);
+  }
+  const float sum = warp_allsum(part);
+  for (int j = lane; j < n; j += 32) s[j] = __fdiv_rn(s[j], sum);
+  __syncwarp();
+#pragma unroll 1
+  for (int cc = 0; cc < 2; ++cc) {
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      if (cc != 0 || c0 != 0) stage_half32(stage, c0, n, 32 * cc, vp, lane);
+      cp_async_wait_warp();
+      const int j = c0 + lane;
+      if (j < n) {
+        const float p = s[j];
+        const float* vr = stage + lane * 32;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 f = lds_f4(vr + ((c ^ (lane & 7)) << 2));
+          acc[4 * c] = __fadd_rn(acc[4 * c], __fmul_rn(p, f.x));
+          acc[4 * c + 1] = __fadd_rn(acc[4 * c + 1], __fmul_rn(p, f.y));
+          acc[4 * c + 2] = __fadd_rn(acc[4 * c + 2], __fmul_rn(p, f.z));
+          acc[4 * c + 3] = __fadd_rn(acc[4 * c + 3], __fmul_rn(p, f.w));
+        }
+      }
+      __syncwarp();
+    }
+    out[32 * cc + lane] = reduce_scatter32(acc);
+  }
+  __syncwarp();
+}
+
+// Per-warp smem floats of the decoder attention kernels.
+__host__ __device__ constexpr int dec_attn_warp_floats(int dh, int nkeys) {
+  return (dh == 64 ? kStageFloats : 0) + round4(dh) + round4(nkeys);
+}
+
 // Decoder self-attention over the cached prefix (model.cpp:620-660): CTA per
 // hypothesis row, warp per head; key j of row r lives at cache row
 // anc[r][j] of step j. Smem: per-head [q | scores] blocks (16-byte aligned),
@@ -475,8 +678,9 @@ __global__ void __launch_bounds__(256, 3)
   const int dh = DH > 0 ? DH : dh_rt;
   const int t = *d_step;
   const int h = threadIdx.x >> 5, lane = threadIdx.x & 31, heads = blockDim.x >> 5;
-  const int W = round4(dh) + round4(T);
-  float* qs = sm + h * W;
+  const int W = dec_attn_warp_floats(DH > 0 ? DH : dh, T);
+  float* stage = sm + h * W;                                 // [kStageFloats] (DH = 64)
+  float* qs = stage + (DH == 64 ? kStageFloats : 0);
   float* ss = qs + round4(dh);
   float* row = sm + heads * W;                   // [d] context row
   float* red = row + d;                          // [33]
@@ -488,11 +692,12 @@ __global__ void __launch_bounds__(256, 3)
   for (int c = lane; c < dh; c += 32) qs[c] = q[c];
   __syncthreads();
   const float* kb = cache + d + h * dh;
-  attend_warp<DH>(
-      qs, t + 1, dh, scale,
-      [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; },
-      [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d; }, ss,
-      row + h * dh);
+  auto kp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; };
+  auto vp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d; };
+  if constexpr (DH == 64)
+    attend_warp_staged64(qs, t + 1, scale, kp, vp, stage, ss, row + h * dh);
+  else
+    attend_warp<DH>(qs, t + 1, dh, scale, kp, vp, ss, row + h * dh);
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
@@ -515,16 +720,20 @@ __global__ void __launch_bounds__(256, 3)
   const int s = row_sent[r];
   const float* kv = ckv + static_cast<long long>(enc_off[s]) * 2 * d + h * dh;
   const int n = enc_len[s];
-  const int W = round4(dh) + round4(max_src);
-  float* qs = sm + h * W;
+  const int W = dec_attn_warp_floats(DH > 0 ? DH : dh, max_src);
+  float* stage = sm + h * W;
+  float* qs = stage + (DH == 64 ? kStageFloats : 0);
   float* ss = qs + round4(dh);
   float* row = sm + heads * W;
   float* red = row + d;
   for (int c = lane; c < dh; c += 32) qs[c] = cq[r * ldq + h * dh + c];
   __syncwarp();
-  attend_warp<DH>(
-      qs, n, dh, scale, [&](int j) { return kv + static_cast<long long>(j) * 2 * d; },
-      [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; }, ss, row + h * dh);
+  auto kp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d; };
+  auto vp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; };
+  if constexpr (DH == 64)
+    attend_warp_staged64(qs, n, scale, kp, vp, stage, ss, row + h * dh);
+  else
+    attend_warp<DH>(qs, n, dh, scale, kp, vp, ss, row + h * dh);
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
@@ -532,6 +741,21 @@ __global__ void __launch_bounds__(256, 3)
 }  // namespace
 
 // ---- launchers ------------------------------------------------------------------------------
+
+namespace {
+// Raises a kernel's dynamic shared memory limit (once per size increase).
+void set_smem_limit(const void* fn, size_t bytes, const char* what) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  if (bytes > 227 * 1024) fail(kUsageError, std::string(what) + ": shared memory too large");
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cur[fn];
+  if (bytes <= 48 * 1024 || bytes <= c) return;
+  MTG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+  c = bytes;
+}
+}  // namespace
 
 void launch_embed_src(const int* ids, const int* pos, int rows, const float* table, int d,
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st) {
@@ -546,6 +770,23 @@ void launch_embed_tgt(const int* prev, const int* d_rows, int max_rows, const in
   if (max_rows <= 0) return;
   launch_k(embed_tgt_kernel, max_rows, 128, 0, st, prev, d_rows, d_step, table, table_q, q_scale, d,
                                              sqrt_d, pe, out, ldo);
+  MTG_CUDA(cudaGetLastError());
+}
+
+void launch_step_begin(const StepBegin& sb, int max_rows, const float* g, const float* b,
+                       const OperandOut& op, cudaStream_t st) {
+  if (max_rows <= 0) return;
+  const int wpb = 4;
+  const dim3 grid((max_rows + wpb - 1) / wpb), block(wpb * 32);
+  const int kpl = (sb.d + 31) / 32;
+  if (kpl <= 1)
+    launch_k(step_begin_kernel<1>, grid, block, 0, st, sb, g, b, op);
+  else if (kpl <= 4)
+    launch_k(step_begin_kernel<4>, grid, block, 0, st, sb, g, b, op);
+  else if (kpl <= 16)
+    launch_k(step_begin_kernel<16>, grid, block, 0, st, sb, g, b, op);
+  else
+    fail(kUsageError, "step_begin: d_model above 512");
   MTG_CUDA(cudaGetLastError());
 }
 
@@ -622,8 +863,9 @@ void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const i
   if (r_max <= 0) return;
   const int dh = d / heads;
   if (heads > 32) fail(kUsageError, "attention: at most 32 heads");
-  const size_t smem = sizeof(float) * (size_t(heads) * (round4(dh) + round4(T)) + d + 33 + T);
+  const size_t smem = sizeof(float) * (size_t(heads) * dec_attn_warp_floats(dh, T) + d + 33 + T);
   auto k = dh == 64 ? dec_self_attention_kernel<64> : dec_self_attention_kernel<0>;
+  set_smem_limit(reinterpret_cast<const void*>(k), smem, "decoder self-attention");
   launch_k(k, r_max, heads * 32, smem, st, qkv_cache, r_max, T, anc0, anc1, d_rows, d_step, d, dh,
            scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
@@ -637,8 +879,9 @@ void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv
   if (max_rows <= 0) return;
   const int dh = d / heads;
   if (heads > 32) fail(kUsageError, "attention: at most 32 heads");
-  const size_t smem = sizeof(float) * (size_t(heads) * (round4(dh) + round4(max_src)) + d + 33);
+  const size_t smem = sizeof(float) * (size_t(heads) * dec_attn_warp_floats(dh, max_src) + d + 33);
   auto k = dh == 64 ? dec_cross_attention_kernel<64> : dec_cross_attention_kernel<0>;
+  set_smem_limit(reinterpret_cast<const void*>(k), smem, "decoder cross-attention");
   launch_k(k, max_rows, heads * 32, smem, st, cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows,
            max_src, d, dh, scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());

@@ -34,6 +34,28 @@ void launch_embed_src(const int* ids, const int* pos, int rows, const float* tab
 
 // Decoder input rows (d_rows on device), position = *d_step. table_q != null:
 // int8 table dequantised as q / scale (model.cpp:485).
+// Fused first kernel of a decode step (kernels.cu step_begin_kernel):
+// history reorder + target embedding + the first decoder LayerNorm.
+struct StepBegin {
+  const int* d_rows;
+  const int* d_step;
+  const int* prev;        // [R] previous token per row
+  const float* table;     // fp32 target embedding (or null with table_q)
+  const int8_t* table_q;  // int8 target embedding
+  float q_scale;
+  float sqrt_d;
+  const float* pe;
+  int d;
+  float* x;  // residual stream [R x ldx]
+  long long ldx;
+  int reorder;  // copy histories from row_parent (beam search) when step >= 1
+  const int* row_parent;
+  int* anc[2];
+  int* tok[2];
+  int T;
+};
+void launch_step_begin(const StepBegin& sb, int max_rows, const float* g, const float* b,
+                       const OperandOut& op, cudaStream_t st);
 void launch_embed_tgt(const int* prev, const int* d_rows, int max_rows, const int* d_step,
                       const float* table, const int8_t* table_q, float q_scale, int d,
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st);

@@ -287,3 +287,47 @@ def test_ragged_lengths_batch_bit_exact():
     for s, h in zip(srcs, hyps):
         r = om.beam_search(s, 5, derive(s, 128), 1.0, True)
         assert (h.tokens, f32hex(h.logprob)) == (r["tokens"], f32hex(r["logprob"]))
+
+
+def test_topk_ties_across_slices_bit_exact(tmp_path):
+    """Duplicated output-embedding rows make many logits tie across the
+    32-column slices: the softmax/top-k merge must rescan every tied slice
+    (long-list path) and still rank by (score desc, token asc)."""
+    c = cfg(1, 1, 16, 32, 2, 20, 2000, 32)
+    om = o.OracleModel.create(c, seed=11)
+    te = om.get("tgt_embed", (2000, 16))
+    om.set("tgt_embed", np.ascontiguousarray(te[np.arange(2000) % 7]))
+    p = str(tmp_path / "ties.bin")
+    om.save(p)
+    srcs = o.synthetic_sources(6, 6, 20, seed=4)
+    gm8 = mt.Model.load(p, precision=mt.INT8)
+    for s, h in zip(srcs, gm8.translate(srcs, mt.BeamConfig(5, 0, 1.0))):
+        r = om.beam_search(s, 5, derive(s, 32), 1.0, True)
+        assert h.tokens == r["tokens"]
+        assert f32hex(h.logprob) == f32hex(r["logprob"])
+    gm32 = mt.Model.load(p, precision=mt.F32)
+    for s, h in zip(srcs, gm32.translate(srcs, mt.BeamConfig(5, 0, 1.0))):
+        assert h.tokens == om.beam_search(s, 5, derive(s, 32), 1.0, False)["tokens"]
+
+
+def test_step_fusion_modes_agree():
+    """The decode-step start can run as three kernels (default) or fused
+    (MTG_STEP_FUSION=1/2); every mode gives the same bits."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2008_04885_b200 as mt, oracle_lib as o\n"
+        "from golden_util import f32hex\n"
+        "c = dict(num_encoder_layers=2, num_decoder_layers=2, d_model=64, d_ff=256, num_heads=4,"
+        " src_vocab_size=700, tgt_vocab_size=900, dropout=0.0, max_seq_len=64)\n"
+        "gm = mt.Model.create(c, seed=3, precision=mt.INT8)\n"
+        "srcs = o.synthetic_sources(6, 9, 700, seed=2)\n"
+        "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs, mt.BeamConfig(5, 0, 1.0))])\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("0", "1", "2"):
+        env = dict(os.environ, MTG_STEP_FUSION=mode)
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
+                                   capture_output=True, text=True).stdout)
+    assert outs[0] == outs[1] == outs[2] and outs[0].strip()
