@@ -157,6 +157,7 @@ Engine::Engine(HostModel model, int precision, int device)
     fail(kUsageError, "unknown precision " + std::to_string(prec_));
   if (host_.quantized && prec_ != kINT8) prec_ = kINT8;  // tools/minimt.cpp:317-320
   if (const char* e = std::getenv("MTG_DIAG_EVENTS")) diag_ = e[0] == '1';
+  if (const char* e = std::getenv("MTG_NO_SPLIT_K")) split_k_ = e[0] != '1';
   if (prec_ == kINT8 && !host_.quantized) quantize_weights(host_);
   const ModelConfig& c = host_.config;
   c.validate();
@@ -406,7 +407,8 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   auto& cache = plan_cache(this);
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
-  if (it == cache.end()) it = cache.emplace(key, plan_gemm(a.op(), w.op(), m, w.n)).first;
+  if (it == cache.end())
+    it = cache.emplace(key, plan_gemm(a.op(), w.op(), m, w.n, 0, 32, split_k_)).first;
   GemmEpilogue ep{};
   ep.C = c;
   ep.ldc = ldc;

@@ -160,6 +160,7 @@ class Engine {
   DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;
   DeviceBuffer<float> part_m_, part_s_;  // [r_max x part_ld_] softmax partials
   DeviceBuffer<int> part_arg_;
+  bool split_k_ = true;
   long long part_ld_ = 0;
   std::vector<DeviceBuffer<float>> qkv_cache_;
   DeviceBuffer<int> src_ids_, src_pos_, src_off_, enc_off_, enc_len_, src_rowseg_;

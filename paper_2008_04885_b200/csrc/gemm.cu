@@ -56,15 +56,35 @@ void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  dim3 grid(p.n_tiles, p.m_tiles);
-  launch_k(gemm_tc_kernel<PREC, BN, EPI>, grid, kGemmThreads, p.smem, stream, p.a, p.b, p.a2,
-           p.b2, p.num_kb, p.nst, ep);
+  dim3 grid(p.n_tiles, p.m_tiles, p.splits);
+  if (p.splits > 1) {  // split-K: the z splits of a tile form one cluster
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = p.splits;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    MTG_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<PREC, BN, EPI>, p.a, p.b, p.a2, p.b2,
+                                p.num_kb, p.nst, ep));
+  } else {
+    launch_k(gemm_tc_kernel<PREC, BN, EPI>, grid, kGemmThreads, p.smem, stream, p.a, p.b, p.a2,
+             p.b2, p.num_kb, p.nst, ep);
+  }
   MTG_CUDA(cudaGetLastError());
 }
 
 template <int PREC>
 void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
   if (ep.part_m) {
+    if (p.splits > 1) fail(kStateError, "gemm: softmax partials cannot be split over K");
     if (ep.bias || ep.residual || ep.relu || ep.d_step)
       fail(kStateError, "gemm: softmax-partials epilogue takes no bias/relu/residual");
     if (ep.part_ld % 4 != 0 || ep.part_ld * 32 < ep.N)
@@ -87,7 +107,7 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
 }  // namespace
 
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn,
-                   int min_bn) {
+                   int min_bn, bool allow_split) {
   if (a.prec != b.prec || a.k_pad != b.k_pad)
     fail(kShapeError, "gemm: operand precision / K mismatch");
   if (a.k_pad % (128 / prec_elem_bytes(a.prec)) != 0)
@@ -109,14 +129,29 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   }
   p.bn = bn;
   p.n_tiles = (n + bn - 1) / bn;
+  // Split-K over a z cluster when the output tiles cannot fill the SMs and a
+  // tile's K stream is long (the DSMEM reduction costs ~1 us): aim for
+  // >= ~160 KB of operand bytes per split, at most 8 (portable cluster).
+  const int tiles = p.m_tiles * p.n_tiles;
+  const long long tile_bytes = static_cast<long long>(p.num_kb) * gemm_stage_bytes(a.prec, bn);
+  const int by_bytes = static_cast<int>((tile_bytes + 160 * 1024 - 1) / (160 * 1024));
+  if (allow_split && tiles < 148 && p.num_kb >= 4 && by_bytes > 1)
+    p.splits = std::max(1, std::min({p.num_kb / 2, 148 / tiles, 8, by_bytes}));
   // Pipeline depth: no deeper than the K loop, and shallow enough for two
-  // CTAs per SM when the tile allows it (epilogue / mainloop overlap).
+  // CTAs per SM when the tile allows it (epilogue / mainloop overlap, and the
+  // next kernel's CTAs can start under PDL; measured: a one-CTA-per-SM depth
+  // is slower even for single-wave grids).
   const int stage = gemm_stage_bytes(a.prec, bn);
   const int want = std::min(kMaxStages, std::max(2, p.num_kb));
   const int two_per_sm = (113 * 1024 - kGemmSmemExtra) / stage;
   const int one_per_sm = (227 * 1024 - kGemmSmemExtra) / stage;
   p.nst = std::min(want, two_per_sm >= 2 ? two_per_sm : one_per_sm);
   if (p.nst < 2 || p.nst * stage < kEpiStageBytes) fail(kStateError, "gemm: tile too large");
+  if (p.splits > 1) {  // the parked split-K partial tile follows the epilogue staging
+    const int need = kEpiStageBytes + 128 * (bn + 4) * 4;
+    while (p.nst * stage < need && p.nst < one_per_sm) ++p.nst;
+    if (p.nst * stage < need) p.splits = 1;
+  }
   p.smem = p.nst * stage + kGemmSmemExtra;
   p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, bn);

@@ -32,15 +32,18 @@ struct GemmPlan {
   int num_kb = 0;
   int m_tiles = 0;
   int n_tiles = 0;
-  int nst = 0;   // pipeline stages
-  int smem = 0;  // dynamic shared memory bytes
+  int nst = 0;     // pipeline stages
+  int smem = 0;    // dynamic shared memory bytes
+  int splits = 1;  // split-K factor (grid.z)
 };
+
 
 // Plans C[M x N] = A[M x K] . B[N x K]^T for at most m_max rows of A.
 // min_bn: smallest tile width the planner may pick (the softmax-partials
 // epilogue needs >= 128).
+// allow_split: pick a split-K factor when the tile grid cannot fill the GPU.
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n,
-                   int force_bn = 0, int min_bn = 32);
+                   int force_bn = 0, int min_bn = 32, bool allow_split = false);
 void launch_gemm(const GemmPlan& plan, const GemmEpilogue& ep, cudaStream_t stream);
 
 }  // namespace mtg

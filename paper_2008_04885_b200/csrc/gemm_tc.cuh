@@ -102,6 +102,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
 
   const int m0 = blockIdx.y * 128;
   const int n0 = blockIdx.x * BN;
+  // Split-K: this CTA's contiguous range of 128-byte K slabs.
+  const int splits = gridDim.z, z = blockIdx.z;
+  const int kb_begin = z * (num_kb / splits) + min(z, num_kb % splits);
+  const int kb_count = num_kb / splits + (z < num_kb % splits ? 1 : 0);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -137,12 +141,33 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // Everything above overlaps the previous kernel (PDL); from here on we read
-  // its outputs (A operand, row count, residual).
+  // Weights (B) do not depend on the previous kernel: the producer starts
+  // their first stages before the programmatic-dependency wait, so the weight
+  // fetch overlaps the predecessor's tail. Everything that reads predecessor
+  // outputs (A operand, row count, scales, residual) comes after pdl_wait.
+  constexpr int kABytes = kATile * (kSplit ? 2 : 1);
+  constexpr int kBBytes = kBTile * (kSplit ? 2 : 1);
+  const int npre = min(nst, kb_count);
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < npre; ++kb) {
+      uint8_t* st = smem + kb * kStageBytes;
+      const int kx = (kb_begin + kb) * kKbElems;
+      mbar_expect_tx(&full_bar[kb], kBBytes);
+      tma_load_2d(st + kATile, &mapB, &full_bar[kb], kx, n0);
+      if constexpr (kSplit) tma_load_2d(st + 2 * kATile + kBTile, &mapB2, &full_bar[kb], kx, n0);
+    }
+  }
   pdl_wait();
   pdl_trigger();
   const int M = ep.d_M ? *ep.d_M : ep.M;
   if (m0 >= M) {  // uniform across the CTA
+    if (warp == 0 && lane == 0) {  // let the prefetched weight stages land first
+      for (int kb = 0; kb < npre; ++kb) {
+        mbar_arrive(&full_bar[kb]);
+        mbar_wait(&full_bar[kb], 0);
+      }
+    }
+    __syncwarp();
     if (warp == 0) tmem_dealloc<kTmemCols>(tmem);
     return;
   }
@@ -150,26 +175,37 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer ----
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = 0; kb < kb_count; ++kb) {
         const int s = kb % nst;
         const uint32_t ph = (kb / nst) & 1;
-        if (kb >= nst) mbar_wait(&empty_bar[s], ph ^ 1);
+        const int kx = (kb_begin + kb) * kKbElems;
         uint8_t* st = smem + s * kStageBytes;
+        if (kb < npre) {  // B already in flight
+          mbar_arrive_expect_tx(&full_bar[s], kABytes);
+          tma_load_2d(st, &mapA, &full_bar[s], kx, m0);
+          if constexpr (kSplit) tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kx, m0);
+          continue;
+        }
+        mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-        tma_load_2d(st, &mapA, &full_bar[s], kb * kKbElems, m0);
-        tma_load_2d(st + kATile, &mapB, &full_bar[s], kb * kKbElems, n0);
+        tma_load_2d(st, &mapA, &full_bar[s], kx, m0);
+        tma_load_2d(st + kATile, &mapB, &full_bar[s], kx, n0);
         if constexpr (kSplit) {
-          tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kb * kKbElems, m0);
-          tma_load_2d(st + 2 * kATile + kBTile, &mapB2, &full_bar[s], kb * kKbElems,
-                      n0);
+          tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kx, m0);
+          tma_load_2d(st + 2 * kATile + kBTile, &mapB2, &full_bar[s], kx, n0);
         }
       }
+    }
+    __syncwarp();
+    if (splits > 1) {  // split-K cluster barriers (1) and (2), see the epilogue
+      cluster_sync_all();
+      cluster_sync_all();
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---- MMA issuer ----
       constexpr uint32_t idesc = make_idesc(kKind, 128, BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = 0; kb < kb_count; ++kb) {
         const int s = kb % nst;
         const uint32_t ph = (kb / nst) & 1;
         mbar_wait(&full_bar[s], ph);
@@ -195,6 +231,11 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       }
       tc_commit(accum_bar);        // accumulator complete
     }
+    __syncwarp();
+    if (splits > 1) {
+      cluster_sync_all();
+      cluster_sync_all();
+    }
   } else {
     // ---- epilogue: TMEM -> registers -> smem transpose -> coalesced global ----
     // Phase 1 (thread = row): convert a 32 x kChunk accumulator sub-tile
@@ -206,7 +247,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     const int half = (warp - 2) >> 2;
     float* stage = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * 33);
     const int rbase = m0 + q * 32;
-    const int nrows = min(32, M - rbase);  // warp-uniform, may be <= 0
+    int nrows = min(32, M - rbase);  // warp-uniform, may be <= 0
     float inv[kMaxSegments];
     if constexpr (PREC == kPrecI8) {
       const float sa = lane < nrows ? ep.a_scale[rbase + lane] : 1.0f;
@@ -245,17 +286,69 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     int sub_a[kSubs];
     mbar_wait(accum_bar, 0);
     tc_fence_after();
+    // Split-K over a thread-block cluster along z: every split parks its raw
+    // accumulator tile in its own (drained) shared memory, then split 0 reads
+    // the others through DSMEM, sums them in z order (int32 exact, float
+    // ordered) and runs the epilogue. Two cluster barriers bracket the reads.
+    constexpr int kPartPitch = BN + 4;  // words; conflict-free row-per-thread float4
+    uint32_t* part = reinterpret_cast<uint32_t*>(smem + kEpiStageBytes);
+    const uint32_t* my_part_row = part + (q * 32 + lane) * kPartPitch;
+    if (splits > 1) {
+#pragma unroll 1
+      for (int c = half * kHalf; c < (half + 1) * kHalf; c += kChunk) {
+        uint32_t r[32];
+        if constexpr (kChunk == 32) {
+          tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, r);
+        } else {
+          tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c,
+                    *reinterpret_cast<uint32_t(*)[16]>(r));
+        }
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < kChunk; j += 4)
+          *reinterpret_cast<uint4*>(part + (q * 32 + lane) * kPartPitch + c + j) =
+              make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
+      }
+      cluster_sync_all();  // (1) all partials parked
+      if (z != 0) nrows = 0;  // only split 0 runs the epilogue
+    }
 #pragma unroll 1
     for (int c = half * kHalf; c < (half + 1) * kHalf; c += kChunk) {
+      if (nrows <= 0) break;  // warp-uniform
       uint32_t r[32];
-      if constexpr (kChunk == 32) {
+      if (splits > 1) {
+        const uint32_t my_addr = smem_u32(my_part_row + c);
+#pragma unroll
+        for (int j = 0; j < kChunk; j += 4) {
+          uint4 a = *reinterpret_cast<const uint4*>(my_part_row + c + j);
+          for (int zz = 1; zz < splits; ++zz) {
+            const uint4 b = dsmem_ld4(dsmem_map(my_addr + 4 * j, zz));
+            if constexpr (PREC == kPrecI8) {
+              a.x += b.x;
+              a.y += b.y;
+              a.z += b.z;
+              a.w += b.w;
+            } else {
+              a.x = __float_as_uint(__fadd_rn(__uint_as_float(a.x), __uint_as_float(b.x)));
+              a.y = __float_as_uint(__fadd_rn(__uint_as_float(a.y), __uint_as_float(b.y)));
+              a.z = __float_as_uint(__fadd_rn(__uint_as_float(a.z), __uint_as_float(b.z)));
+              a.w = __float_as_uint(__fadd_rn(__uint_as_float(a.w), __uint_as_float(b.w)));
+            }
+          }
+          r[j] = a.x;
+          r[j + 1] = a.y;
+          r[j + 2] = a.z;
+          r[j + 3] = a.w;
+        }
+      } else if constexpr (kChunk == 32) {
         tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, r);
+        tmem_ld_wait();
       } else {
         tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c,
                   *reinterpret_cast<uint32_t(*)[16]>(r));
+        tmem_ld_wait();
       }
-      tmem_ld_wait();
-      if (nrows <= 0 || n0 + c >= N) continue;  // warp-uniform
+      if (n0 + c >= N) continue;  // warp-uniform
       float v[kChunk];
       if constexpr (PREC == kPrecI8) {
         if (ep.seg_width == 0 || ep.seg_width % kChunk == 0) {
@@ -393,6 +486,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         }
       }
     }
+    if (splits > 1) cluster_sync_all();  // (2) split 0 is done reading the partials
   }
 
   tc_fence_before();
