@@ -31,7 +31,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libminimt_gpu.so")
+# MTG_LIB_PATH overrides the library (A/B builds); default: the in-tree build.
+LIB_PATH = os.environ.get("MTG_LIB_PATH") or os.path.join(_HERE, "libminimt_gpu.so")
 
 F32, BF16, INT8 = 0, 1, 2
 PAD_ID, UNK_ID, BOS_ID, EOS_ID = 0, 1, 2, 3  # model.hpp:16-19
@@ -108,7 +109,8 @@ def _load():
     lib.mtg_translate_staged.argtypes = [c_void_p, c_void_p]
     lib.mtg_last_launch_count.argtypes = [c_void_p]
     lib.mtg_last_launch_count.restype = ctypes.c_int64
-    lib.mtg_diag_report.argtypes = [c_void_p, ctypes.c_char_p, ctypes.c_size_t]
+    if hasattr(lib, "mtg_diag_report"):  # absent in older A/B builds
+        lib.mtg_diag_report.argtypes = [c_void_p, ctypes.c_char_p, ctypes.c_size_t]
     return lib
 
 

@@ -302,6 +302,7 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   rowmax_.resize(act_rows_);
   src_pos_.resize(M);
   src_off_.resize(N + 1);
+  sent_absmax_.resize(N);
   enc_off_.resize(N);
   enc_len_.resize(N);
   nonfinite_.resize(1);
@@ -403,7 +404,7 @@ void Engine::prep(const float* x, long long ldx, int k, int max_rows, const int*
 
 void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
                   long long ldc, const float* bias, const float* residual, int relu,
-                  long long c_step_stride, const int* d_step) {
+                  long long c_step_stride, const int* d_step, unsigned* seg_absmax) {
   auto& cache = plan_cache(this);
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
@@ -424,13 +425,28 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   ep.M = m;
   ep.d_M = d_m;
   ep.N = w.n;
+  if (seg_absmax) {
+    if (residual) fail(kStateError, "gemm: sentence-max epilogue takes no residual");
+    ep.seg_absmax = seg_absmax;
+    ep.row_seg = src_rowseg_.get();
+    ep.nonfinite = nonfinite_.get();
+  }
   launch_gemm(it->second, ep, stream_);
-  count(w.n == 3 * d_ ? "gemm qkv" : w.n == 2 * d_ ? "gemm kv" : w.n == dff_ ? "gemm w1"
-        : w.k == dff_ ? "gemm w2" : "gemm d x d");
+  if (enc_diag_active_)
+    count(w.n == 3 * d_ ? "enc gemm qkv" : w.n == 2 * d_ ? "enc gemm cross kv"
+          : w.n == dff_ ? "enc gemm w1" : w.k == dff_ ? "enc gemm w2" : "enc gemm d x d");
+  else
+    count(w.n == 3 * d_ ? "gemm qkv" : w.n == 2 * d_ ? "gemm kv" : w.n == dff_ ? "gemm w1"
+          : w.k == dff_ ? "gemm w2" : "gemm d x d");
 }
 
 void Engine::count(const char* tag) {
   ++launches_;
+  if (diag_ && enc_diag_active_) {
+    enc_marks_.push_back({tag, nullptr});
+    MTG_CUDA(cudaEventCreate(&enc_marks_.back().ev));
+    MTG_CUDA(cudaEventRecord(enc_marks_.back().ev, stream_));
+  }
   if (diag_ && capturing_) {
     diag_marks_.push_back({tag, nullptr});
     MTG_CUDA(cudaEventCreate(&diag_marks_.back().ev));
@@ -444,6 +460,9 @@ void Engine::diag_clear() {
   diag_marks_.clear();
   diag_ms_.clear();
   diag_steps_ = 0;
+  enc_agg_.clear();
+  enc_total_ms_ = 0.0;
+  enc_runs_ = 0;
 }
 
 std::string Engine::diag_report() const {
@@ -459,7 +478,20 @@ std::string Engine::diag_report() const {
   }
   char tl[96];
   std::snprintf(tl, sizeof tl, "total per step %.2f us\n", 1000.0 * total / diag_steps_);
-  return out + tl;
+  out += tl;
+  if (enc_runs_ > 0) {
+    out += "encoder (per run, " + std::to_string(enc_runs_) + " runs)\n";
+    for (const auto& [tag, v] : enc_agg_) {
+      char line[160];
+      std::snprintf(line, sizeof line, "    %-32s %9.2f us  %4d launches  %7.2f us each\n",
+                    tag.c_str(), 1000.0 * v.first / enc_runs_, v.second / enc_runs_,
+                    1000.0 * v.first / v.second);
+      out += line;
+    }
+    std::snprintf(tl, sizeof tl, "encoder total %.2f us\n", 1000.0 * enc_total_ms_ / enc_runs_);
+    out += tl;
+  }
+  return out;
 }
 
 void Engine::gemm_logits(int m, const int* d_m) {
@@ -545,11 +577,11 @@ void Engine::prep_enc(const float* x, long long ldx, int k, int m, ActOperand& o
   if (prec_ == kINT8) {
     if (!have_rowmax) {
       launch_rowmax(x, ldx, m, k, rowmax_.get(), nonfinite_.get(), stream_);
-      count();
+      count("enc rowmax");
     }
     launch_quantize_seg(x, ldx, m, k, src_rowseg_.get(), src_off_.get(), rowmax_.get(),
                         opout(out), stream_);
-    count();
+    count("enc quantize_seg");
   } else {
     prep(x, ldx, k, m, nullptr, nullptr, 0, out);
   }
@@ -557,39 +589,95 @@ void Engine::prep_enc(const float* x, long long ldx, int k, int m, ActOperand& o
 
 // Encoder LayerNorm; int8 also records per-row max |y| for the segment scale.
 void Engine::ln_enc(const float* x, int m, const LN& ln, float* y, ActOperand& out) {
+  if (prec_ == kINT8 && enc_fused_) {  // fused LN + per-sentence quantization
+    launch_ln_quant_sent(x, d_, src_off_.get(), enc_n_sent_, d_, ln.g.get(), ln.b.get(), y, d_,
+                         opout(out), sent_absmax_.get(), stream_);
+    count("enc layernorm+quantize");
+    return;
+  }
   if (prec_ == kINT8) {
     launch_layernorm(x, d_, m, nullptr, d_, ln.g.get(), ln.b.get(), y, d_, rowmax_.get(),
                      nullptr, stream_);
-    count();
+    count("enc layernorm");
     prep_enc(y, d_, d_, m, out, true);
   } else {
     const OperandOut o = opout(out);
     launch_layernorm(x, d_, m, nullptr, d_, ln.g.get(), ln.b.get(), y, d_, nullptr, &o, stream_);
-    count();
+    count("enc layernorm");
   }
 }
 
 void Engine::run_encoder(int n_sent, int m, int max_src) {
   if (m <= 0) return;
+  if (diag_ && !capturing_) {
+    enc_diag_active_ = true;
+    enc_marks_.push_back({"start", nullptr});
+    MTG_CUDA(cudaEventCreate(&enc_marks_.back().ev));
+    MTG_CUDA(cudaEventRecord(enc_marks_.back().ev, stream_));
+  }
+  run_encoder_body(n_sent, m, max_src);
+  if (enc_diag_active_) {
+    enc_diag_active_ = false;
+    MTG_CUDA(cudaStreamSynchronize(stream_));
+    for (size_t i = 1; i < enc_marks_.size(); ++i) {
+      float ms = 0.0f;
+      MTG_CUDA(cudaEventElapsedTime(&ms, enc_marks_[i - 1].ev, enc_marks_[i].ev));
+      auto& a = enc_agg_[enc_marks_[i].name];
+      a.first += ms;
+      a.second += 1;
+      enc_total_ms_ += ms;
+    }
+    for (auto& mk : enc_marks_) cudaEventDestroy(mk.ev);
+    enc_marks_.clear();
+    ++enc_runs_;
+  }
+}
+
+void Engine::run_encoder_body(int n_sent, int m, int max_src) {
   const ModelConfig& c = host_.config;
   const long long d = d_;
   const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
   const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
   launch_embed_src(src_ids_.get(), src_pos_.get(), m, src_embed_.get(), d_, sqrt_d, pe_.get(),
                    enc_x_.get(), d, stream_);
-  count();
+  count("enc embed");
+  enc_n_sent_ = n_sent;
+  // int8 with d <= 512: the LayerNorms quantize per sentence themselves and
+  // zero the sentence max that attention / the FFN-up epilogue accumulate,
+  // so each remaining quantize is a single pass (9 kernels per layer).
+  static const bool no_enc_fusion = [] {
+    const char* e = std::getenv("MTG_NO_ENC_FUSION");
+    return e && e[0] == '1';
+  }();
+  const bool fused = prec_ == kINT8 && d_ <= 512 && !no_enc_fusion;
+  enc_fused_ = fused;
+  const OperandOut od = opout(act_d_), off_ = opout(act_ff_);
   for (int l = 0; l < c.num_encoder_layers; ++l) {
     EncLayer& L = enc_[l];
     ln_enc(enc_x_.get(), m, L.n1, enc_a_.get(), act_d_);
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
     launch_enc_attention(enc_qkv_.get(), 3 * d, src_off_.get(), n_sent, std::max(max_src, 1), d_,
-                         heads_, scale, enc_ctx_.get(), d, stream_);
-    count();
-    prep_enc(enc_ctx_.get(), d, d_, m, act_d_, false);
+                         heads_, scale, enc_ctx_.get(), d, fused ? sent_absmax_.get() : nullptr,
+                         nonfinite_.get(), stream_);
+    count("enc attention");
+    if (fused) {
+      launch_quantize_sent(enc_ctx_.get(), d, m, d_, src_rowseg_.get(), sent_absmax_.get(), od,
+                           stream_);
+      count("enc quantize (sentence max)");
+    } else {
+      prep_enc(enc_ctx_.get(), d, d_, m, act_d_, false);
+    }
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
     ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
-    gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
-    prep_enc(ffh_.get(), dff_, dff_, m, act_ff_, false);
+    gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1, 0, nullptr,
+         fused ? sent_absmax_.get() : nullptr);
+    if (fused) {
+      launch_quantize_sent(ffh_.get(), dff_, m, dff_, src_rowseg_.get(), sent_absmax_.get(), off_,
+                           stream_);
+      count("enc quantize (sentence max)");
+    } else {
+      prep_enc(ffh_.get(), dff_, dff_, m, act_ff_, false);
+    }
     gemm(act_ff_, L.w2, m, nullptr, enc_x_.get(), d, L.b2.get(), enc_x_.get(), 0);
   }
   if (c.num_decoder_layers == 0) {

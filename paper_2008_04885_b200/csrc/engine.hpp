@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -100,11 +101,13 @@ class Engine {
   void ln_enc(const float* x, int m, const LN& ln, float* y, ActOperand& out);
   void gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
             long long ldc, const float* bias, const float* residual, int relu,
-            long long c_step_stride = 0, const int* d_step = nullptr);
+            long long c_step_stride = 0, const int* d_step = nullptr,
+            unsigned* seg_absmax = nullptr);
   // Output projection into logits_ plus the per-slice softmax partials.
   void gemm_logits(int m, const int* d_m);
   int stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status);
   void run_encoder(int n_sent, int m_enc, int max_src);
+  void run_encoder_body(int n_sent, int m_enc, int max_src);
   // reorder: beam search (copy histories from row_parent at step >= 1).
   void decoder_body(bool reorder);  // decoder layers + dec_final + logits for the live rows
   void decode_loop(int t_run);
@@ -127,6 +130,11 @@ class Engine {
   std::vector<DiagMark> diag_marks_;
   std::vector<double> diag_ms_;
   int diag_steps_ = 0;
+  bool enc_diag_active_ = false;          // encoder kernels are recorded eagerly
+  std::vector<DiagMark> enc_marks_;
+  std::map<std::string, std::pair<double, int>> enc_agg_;  // tag -> (ms, launches)
+  double enc_total_ms_ = 0.0;
+  int enc_runs_ = 0;
   void diag_clear();
 
   // ---- weights ----
@@ -160,6 +168,9 @@ class Engine {
   DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;
   DeviceBuffer<float> part_m_, part_s_;  // [r_max x part_ld_] softmax partials
   DeviceBuffer<int> part_arg_;
+  DeviceBuffer<unsigned> sent_absmax_;  // per-sentence max |x| (float bits), encoder int8
+  int enc_n_sent_ = 0;
+  bool enc_fused_ = false;
   bool split_k_ = true;
   long long part_ld_ = 0;
   std::vector<DeviceBuffer<float>> qkv_cache_;

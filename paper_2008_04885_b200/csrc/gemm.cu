@@ -95,6 +95,15 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
     }
     fail(kStateError, "gemm: softmax partials need a 128/256-column tile");
   }
+  if (ep.seg_absmax) {
+    if (ep.residual) fail(kStateError, "gemm: segment-max epilogue takes no residual");
+    switch (p.bn) {
+      case 32: return launch_one<PREC, 32, kEpiSegMax>(p, ep, stream);
+      case 64: return launch_one<PREC, 64, kEpiSegMax>(p, ep, stream);
+      case 128: return launch_one<PREC, 128, kEpiSegMax>(p, ep, stream);
+      case 256: return launch_one<PREC, 256, kEpiSegMax>(p, ep, stream);
+    }
+  }
   switch (p.bn) {
     case 32: return launch_one<PREC, 32, kEpiLinear>(p, ep, stream);
     case 64: return launch_one<PREC, 64, kEpiLinear>(p, ep, stream);

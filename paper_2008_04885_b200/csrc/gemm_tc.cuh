@@ -53,12 +53,19 @@ struct GemmEpilogue {
   float* part_s;
   int* part_arg;
   long long part_ld;
+  // Per-segment max |output| (float bits, atomicMax) for a following int8
+  // quantize with one scale per sentence; bias and ReLU then apply in the
+  // row-per-thread phase. Segment of row r: row_seg[r].
+  unsigned* seg_absmax;
+  const int* row_seg;
+  int* nonfinite;
 };
 
 // EPI = 0: linear-layer epilogue. EPI = 1: output projection; also emits the
 // log-softmax / top-k partials (no bias, relu or residual).
 constexpr int kEpiLinear = 0;
 constexpr int kEpiSoftmaxParts = 1;
+constexpr int kEpiSegMax = 2;  // linear + per-segment max |y| (bias/ReLU in phase 1)
 
 enum GemmPrec : int { kPrecI8 = 0, kPrecBF16 = 1, kPrecTF32x3 = 2 };
 
@@ -261,13 +268,16 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         ep.d_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride : 0LL;
     const bool has_bias = ep.bias != nullptr, has_res = ep.residual != nullptr;
     const bool relu = ep.relu != 0;
+    constexpr bool seg_mode = EPI == kEpiSegMax;  // host: no residual
+    float seg_max = 0.0f;
+    int seg_bad = 0;
     const int N = ep.N;
     const long long ldc = ep.ldc, ldr = ep.ldr;
     float* const Cbase = ep.C + step_off + static_cast<long long>(rbase) * ldc;
     // BN = 32 (the N = d_model residual GEMMs): each epilogue warp owns one
     // 32-row x 16-column chunk, so its residual and bias are fetched while
     // the MMAs are still running.
-    constexpr bool kPrefetch = (BN == 32 && EPI == kEpiLinear);
+    constexpr bool kPrefetch = (BN == 32 && EPI != kEpiSoftmaxParts);
     float res_pre[kPrefetch ? 32 : 1];
     float bias_pre = 0.0f;
     if constexpr (kPrefetch) {
@@ -374,6 +384,20 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(r[j]);
       }
+      if constexpr (seg_mode) {  // bias + ReLU here, row max for the sentence scale
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int col = n0 + c + j;
+          if (col < N) {
+            float x = v[j];
+            if (has_bias) x = __fadd_rn(x, ep.bias[col]);
+            if (relu) x = x > 0.0f ? x : 0.0f;
+            v[j] = x;
+            seg_max = fmaxf(seg_max, fabsf(x));
+            seg_bad |= !isfinite(x);
+          }
+        }
+      }
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) stage[lane * 33 + j] = v[j];
       if constexpr (EPI == kEpiSoftmaxParts) {
@@ -413,15 +437,15 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           float x = stage[i * 33 + (lane % kChunk)];
-          if (has_bias) x = __fadd_rn(x, bias_pre);
-          if (relu) x = x > 0.0f ? x : 0.0f;
+          if (has_bias && !seg_mode) x = __fadd_rn(x, bias_pre);
+          if (relu && !seg_mode) x = x > 0.0f ? x : 0.0f;
           if (has_res) x = __fadd_rn(res_pre[i], x);
           if (col_ok && i < nrows) cp[i * ldc] = x;
         }
         __syncwarp();
         continue;
       }
-      if (EPI == kEpiSoftmaxParts || (!has_bias && !relu && !has_res)) {
+      if (EPI == kEpiSoftmaxParts || (!has_bias && !relu && !has_res) || seg_mode) {
         if (col_ok) {
 #pragma unroll 8
           for (int i = 0; i < 32; ++i)
@@ -452,6 +476,21 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         }
       }
       __syncwarp();
+    }
+    if (seg_mode && nrows > 0) {  // constexpr-false for the other epilogues
+      // Segmented max over the warp's rows (segments are contiguous row
+      // ranges), then one atomic per segment present in the warp.
+      const int sg = lane < nrows ? ep.row_seg[rbase + lane] : -1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float ov = __shfl_down_sync(0xffffffffu, seg_max, o);
+        const int os = __shfl_down_sync(0xffffffffu, sg, o);
+        if (lane + o < 32 && os == sg) seg_max = fmaxf(seg_max, ov);
+      }
+      const int prev = __shfl_up_sync(0xffffffffu, sg, 1);
+      if (__any_sync(0xffffffffu, seg_bad) && lane == 0) atomicExch(ep.nonfinite, 1);
+      if (sg >= 0 && (lane == 0 || prev != sg))
+        atomicMax(ep.seg_absmax + sg, __float_as_uint(seg_max));
     }
     if constexpr (EPI == kEpiSoftmaxParts) {
       // Row rbase+lane, slices sub0 .. sub0+kSubs-1 (sub0 % kSubs == 0).

@@ -349,6 +349,102 @@ __global__ void quantize_seg_kernel(const float* __restrict__ x, long long ldx, 
   write_operand(op, r, x + r * ldx, n, qscale_of(m), lane, 32);
 }
 
+// Encoder LayerNorm + int8 operand with one scale per sentence (the quantize
+// call tensor is the sentence's [S x d] block, model.cpp:461-466): CTA per
+// sentence. Pass 1 normalises each row (warp per row, P1 sums) into y and
+// tracks max |y|; pass 2 quantizes with 127 / max. Also clears this
+// sentence's abs-max slot for the kernels that accumulate into it later.
+template <int KPL>
+__global__ void __launch_bounds__(1024)
+    ln_quant_sent_kernel(const float* __restrict__ x, long long ldx, const int* __restrict__ off,
+                         int n, const float* __restrict__ g, const float* __restrict__ b,
+                         float* __restrict__ y, long long ldy, OperandOut op,
+                         unsigned* __restrict__ sent_absmax) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int s = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int r0 = off[s], r1 = off[s + 1];
+  float gv[KPL], bv[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    gv[i] = c < n ? g[c] : 0.0f;
+    bv[i] = c < n ? b[c] : 0.0f;
+  }
+  float mx = 0.0f;
+  int bad = 0;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const float* xr = x + r * ldx;
+    float xv[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      xv[i] = c < n ? xr[c] : 0.0f;
+    }
+    float part = 0.0f;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i)
+      if (lane + 32 * i < n) part = __fadd_rn(part, xv[i]);
+    const float nf = static_cast<float>(n);
+    const float mu = __fdiv_rn(warp_allsum(part), nf);
+    float part2 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i)
+      if (lane + 32 * i < n) {
+        const float dv = __fsub_rn(xv[i], mu);
+        part2 = __fadd_rn(part2, __fmul_rn(dv, dv));
+      }
+    const float var = __fdiv_rn(warp_allsum(part2), nf);
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+    float* yr = y + r * ldy;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < n) {
+        const float v = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[i], mu), inv), gv[i]), bv[i]);
+        yr[c] = v;
+        mx = fmaxf(mx, fabsf(v));
+        bad |= !isfinite(v);
+      }
+    }
+  }
+  mx = warp_allmax(mx);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(op.nonfinite, 1);
+  if (lane == 0) red[warp] = mx;
+  if (threadIdx.x == 0 && sent_absmax) sent_absmax[s] = 0u;
+  __syncthreads();
+  float m = lane < nw ? red[lane] : 0.0f;
+  m = warp_allmax(m);
+  const float scale = qscale_of(m);
+  for (int r = r0 + warp; r < r1; r += nw) {  // same warp re-reads its own rows
+    const float* yr = y + r * ldy;
+    int8_t* q = op.q + static_cast<long long>(r) * op.k_pad;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < op.k_pad) q[c] = c < n ? quant1(yr[c], scale) : 0;
+    }
+    for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) q[c] = 0;
+    if (lane == 0) op.row_scale[r] = scale;
+  }
+}
+
+// int8 operand of rows with one scale per sentence, from a per-sentence max
+// |x| accumulated by the producing kernel (float bits, atomicMax).
+__global__ void quantize_sent_kernel(const float* __restrict__ x, long long ldx, int rows, int n,
+                                     const int* __restrict__ row_seg,
+                                     const unsigned* __restrict__ sent_absmax, OperandOut op) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float m = __uint_as_float(sent_absmax[row_seg[r]]);
+  write_operand(op, r, x + r * ldx, n, qscale_of(m), lane, 32);
+}
+
 // ---- attention ---------------------------------------------------------------------------
 
 // Sums 32 per-lane partial vectors: lane l returns sum over lanes of a[l].
@@ -473,7 +569,8 @@ __host__ __device__ constexpr int enc_kv_pitch(int dh) { return dh % 4 == 0 ? dh
 template <int DH>
 __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ldq,
                                      const int* __restrict__ off, int d, int dh_rt, int max_len,
-                                     float scale, float* __restrict__ ctx, long long ldc) {
+                                     float scale, float* __restrict__ ctx, long long ldc,
+                                     unsigned* __restrict__ sent_absmax, int* nonfinite) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) float sm[];
@@ -504,12 +601,26 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
     }
   }
   __syncthreads();
+  float mx = 0.0f;
+  int bad = 0;
   for (int i = warp; i < n; i += nw) {
     for (int c = lane; c < dh; c += 32) qs[c] = base[i * ldq + c];
     __syncwarp();
+    float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
     attend_warp<DH>(
         qs, n, dh, scale, [&](int j) { return Ks + j * P; }, [&](int j) { return Vs + j * P; },
-        ss, ctx + static_cast<long long>(r0 + i) * ldc + h * dh);
+        ss, out);
+    if (sent_absmax) {
+      for (int c = lane; c < dh; c += 32) {  // lane wrote these itself
+        mx = fmaxf(mx, fabsf(out[c]));
+        bad |= !isfinite(out[c]);
+      }
+    }
+  }
+  if (sent_absmax) {  // the quantize call tensor is the sentence's context block
+    mx = warp_allmax(mx);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+    if (lane == 0) atomicMax(sent_absmax + s, __float_as_uint(mx));
   }
 }
 
@@ -822,6 +933,35 @@ void launch_rowmax(const float* x, long long ldx, int rows, int n, float* rowmax
   MTG_CUDA(cudaGetLastError());
 }
 
+void launch_ln_quant_sent(const float* x, long long ldx, const int* off, int n_sent, int n,
+                          const float* g, const float* b, float* y, long long ldy,
+                          const OperandOut& op, unsigned* sent_absmax, cudaStream_t st) {
+  if (n_sent <= 0) return;
+  if (op.prec != 0) fail(kStateError, "ln_quant_sent: int8 operands only");
+  const int kpl = (n + 31) / 32;
+  if (kpl <= 1)
+    launch_k(ln_quant_sent_kernel<1>, n_sent, 1024, 0, st, x, ldx, off, n, g, b, y, ldy, op,
+             sent_absmax);
+  else if (kpl <= 4)
+    launch_k(ln_quant_sent_kernel<4>, n_sent, 1024, 0, st, x, ldx, off, n, g, b, y, ldy, op,
+             sent_absmax);
+  else if (kpl <= 16)
+    launch_k(ln_quant_sent_kernel<16>, n_sent, 1024, 0, st, x, ldx, off, n, g, b, y, ldy, op,
+             sent_absmax);
+  else
+    fail(kUsageError, "ln_quant_sent: d_model above 512");
+  MTG_CUDA(cudaGetLastError());
+}
+
+void launch_quantize_sent(const float* x, long long ldx, int rows, int n, const int* row_seg,
+                          const unsigned* sent_absmax, const OperandOut& op, cudaStream_t st) {
+  if (rows <= 0) return;
+  const int wpb = 8;
+  launch_k(quantize_sent_kernel, (rows + wpb - 1) / wpb, wpb * 32, 0, st, x, ldx, rows, n, row_seg,
+           sent_absmax, op);
+  MTG_CUDA(cudaGetLastError());
+}
+
 void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const int* row_seg,
                          const int* seg_off, const float* rowmax, const OperandOut& op,
                          cudaStream_t st) {
@@ -834,7 +974,7 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
                           int max_len, int d, int heads, float scale, float* ctx, long long ldc,
-                          cudaStream_t st) {
+                          unsigned* sent_absmax, int* nonfinite, cudaStream_t st) {
   if (n_sent <= 0) return;
   const int dh = d / heads;
   const int nw = 8;
@@ -852,7 +992,7 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
     cfg = smem;
   }
   launch_k(k, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale, ctx,
-           ldc);
+           ldc, sent_absmax, nonfinite);
   MTG_CUDA(cudaGetLastError());
 }
 

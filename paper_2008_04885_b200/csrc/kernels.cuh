@@ -81,9 +81,19 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 
 // Encoder self-attention over each sentence (rows off[s]..off[s+1]).
 // qkv rows: [q | k | v] each d wide, pitch ldq. ctx pitch ldc.
+// sent_absmax (optional): max |ctx| per sentence accumulated as float bits
+// (atomicMax) for the per-sentence int8 scale; non-finite values set *nonfinite.
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
-                          int max_len, int d, int heads, float scale, float* ctx,
-                          long long ldc, cudaStream_t st);
+                          int max_len, int d, int heads, float scale, float* ctx, long long ldc,
+                          unsigned* sent_absmax, int* nonfinite, cudaStream_t st);
+// Encoder LayerNorm -> int8 operand with one scale per sentence (CTA per
+// sentence); zeroes sent_absmax[s] for later accumulation.
+void launch_ln_quant_sent(const float* x, long long ldx, const int* off, int n_sent, int n,
+                          const float* g, const float* b, float* y, long long ldy,
+                          const OperandOut& op, unsigned* sent_absmax, cudaStream_t st);
+// int8 operand rows scaled by their sentence's accumulated max |x|.
+void launch_quantize_sent(const float* x, long long ldx, int rows, int n, const int* row_seg,
+                          const unsigned* sent_absmax, const OperandOut& op, cudaStream_t st);
 
 // Decoder self-attention for live row r at step t over positions 0..t; the key
 // of position j lives in row anc[r*T + j] of the step-j slab of qkv_cache
