@@ -498,8 +498,20 @@ void Engine::gemm_logits(int m, const int* d_m) {
   auto& cache = plan_cache(this);
   PlanKey key{act_d_.op().ptr, logits_w_.op().ptr, m};
   auto it = cache.find(key);
+  // Persistent double-buffered kernel for TF32x3 (MMA-bound); the int8 / bf16
+  // projection is epilogue-bound and measured faster as one tile per CTA at
+  // two CTAs per SM. MTG_LOGITS_PERSISTENT=0/1 overrides (A/B).
+  static const int persistent_env = [] {
+    const char* e = std::getenv("MTG_LOGITS_PERSISTENT");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool persistent = persistent_env >= 0 ? persistent_env != 0 : prec_ == kF32;
   if (it == cache.end())
-    it = cache.emplace(key, plan_gemm(act_d_.op(), logits_w_.op(), m, logits_w_.n, 0, 128)).first;
+    it = cache
+             .emplace(key, persistent ? plan_logits(act_d_.op(), logits_w_.op(), m, logits_w_.n)
+                                      : plan_gemm(act_d_.op(), logits_w_.op(), m, logits_w_.n,
+                                                  0, 128))
+             .first;
   GemmEpilogue ep{};
   ep.C = logits_.get();
   ep.ldc = Vp_;

@@ -1,5 +1,6 @@
 // Host side of the tcgen05 GEMM: TMA tensor maps, tile-size choice, launch.
 #include "gemm.hpp"
+#include "logits_tc.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -175,7 +176,61 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   return p;
 }
 
+namespace {
+template <int PREC, int BN, int EG>
+void launch_logits_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    MTG_CUDA(cudaFuncSetAttribute(logits_tc_kernel<PREC, BN, EG>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  const int grid = std::min(148, p.m_tiles * p.n_tiles);
+  launch_k(logits_tc_kernel<PREC, BN, EG>, grid, 64 + EG * 256, p.smem, stream, p.a, p.b, p.a2,
+           p.b2, p.num_kb, p.nst, p.n_tiles, ep);
+  MTG_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+GemmPlan plan_logits(const Operand& a, const Operand& b, int m_max, int n) {
+  if (a.prec != b.prec || a.k_pad != b.k_pad)
+    fail(kShapeError, "logits: operand precision / K mismatch");
+  GemmPlan p;
+  p.prec = a.prec;
+  p.persistent = true;
+  p.num_kb = a.k_pad * prec_elem_bytes(a.prec) / 128;
+  p.m_tiles = (m_max + 127) / 128;
+  p.bn = a.prec == kPrecTF32x3 ? 128 : 256;  // TF32x3 stages are twice as large
+  p.n_tiles = (n + p.bn - 1) / p.bn;
+  const int stage = gemm_stage_bytes(a.prec, p.bn);
+  const int groups = a.prec == kPrecTF32x3 ? 1 : 2;  // must match launch_gemm's instantiation
+  const int budget = 227 * 1024 - groups * kEpiStageBytes - kGemmSmemExtra;
+  p.nst = std::min({kMaxStages, budget / stage, std::max(2, p.num_kb)});
+  if (p.nst < 2) fail(kStateError, "logits: tile too large");
+  p.smem = p.nst * stage + groups * kEpiStageBytes + kGemmSmemExtra;
+  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
+  p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, p.bn);
+  if (a.prec == kPrecTF32x3) {
+    if (!a.ptr_lo || !b.ptr_lo) fail(kStateError, "logits: TF32x3 needs lo operands");
+    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 128);
+    p.b2 = make_map(b.ptr_lo, b.prec, b.rows, b.k_pad, p.bn);
+  } else {
+    p.a2 = p.a;
+    p.b2 = p.b;
+  }
+  return p;
+}
+
 void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  if (p.persistent) {
+    if (!ep.part_m) fail(kStateError, "logits: softmax partial buffers missing");
+    switch (p.prec) {
+      case kPrecI8: return launch_logits_one<kPrecI8, 256, 2>(p, ep, stream);
+      case kPrecBF16: return launch_logits_one<kPrecBF16, 256, 2>(p, ep, stream);
+      case kPrecTF32x3: return launch_logits_one<kPrecTF32x3, 128, 1>(p, ep, stream);
+    }
+    fail(kStateError, "logits: unknown precision");
+  }
   switch (p.prec) {
     case kPrecI8: return launch_prec<kPrecI8>(p, ep, stream);
     case kPrecBF16: return launch_prec<kPrecBF16>(p, ep, stream);

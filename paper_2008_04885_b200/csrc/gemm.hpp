@@ -35,6 +35,7 @@ struct GemmPlan {
   int nst = 0;     // pipeline stages
   int smem = 0;    // dynamic shared memory bytes
   int splits = 1;  // split-K factor (grid.z)
+  bool persistent = false;  // output projection: logits_tc_kernel
 };
 
 
@@ -44,6 +45,9 @@ struct GemmPlan {
 // allow_split: pick a split-K factor when the tile grid cannot fill the GPU.
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n,
                    int force_bn = 0, int min_bn = 32, bool allow_split = false);
+// Output projection with softmax partials (logits_tc.cuh): persistent CTAs,
+// double-buffered TMEM accumulators. Launch with launch_gemm.
+GemmPlan plan_logits(const Operand& a, const Operand& b, int m_max, int n);
 void launch_gemm(const GemmPlan& plan, const GemmEpilogue& ep, cudaStream_t stream);
 
 }  // namespace mtg
