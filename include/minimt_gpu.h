@@ -128,6 +128,33 @@ int mtg_translate(mtg_model* m, const int32_t* src_ids, const int64_t* src_offse
 /* Parity entry for decode_step (model.cpp:614-672): for each sentence, feed
  * BOS + forced[0..n_forced-1) and return the logits of every step,
  * out_logits[(i*n_forced + t)*V + v]. All sentences share n_forced. */
+/* Source factors (model.cpp:539-581, decode.cpp:334-342): factor_ids holds
+ * n_factors streams, each aligned with src_ids (stream f at
+ * factor_ids + f * src_offsets[n_sentences]; same CSR offsets, EOS position
+ * included). n_factors must equal the model's factor count, otherwise the
+ * sentence fails with MTG_SHAPE_ERROR, like embed_source_infer. */
+int mtg_translate_factors(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                          int n_sentences, const int32_t* factor_ids, int n_factors,
+                          const mtg_beam_config* cfg, int32_t* out_tokens, int out_stride,
+                          int32_t* out_len, float* out_logprob, float* out_norm_score,
+                          uint32_t* out_flags, int32_t* out_status);
+int mtg_encode_factors(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                       int n_sentences, const int32_t* factor_ids, int n_factors, float* out);
+
+/* Full form: optional source factors (as above, or NULL / 0) and optional
+ * vocabulary shortlists (decode.cpp:113-165, 344-349; model.cpp:440-449):
+ * sentence s uses target ids shortlist_ids[shortlist_offsets[s] ..
+ * shortlist_offsets[s+1]) -- strictly increasing, < tgt_vocab_size, at most
+ * 4096 -- or the full vocabulary when that range is empty (or the arrays are
+ * NULL). Logits, log-softmax and candidates cover the shortlist only; the
+ * candidate token is the full-vocabulary id. */
+int mtg_translate_ex(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                     int n_sentences, const int32_t* factor_ids, int n_factors,
+                     const int32_t* shortlist_ids, const int64_t* shortlist_offsets,
+                     const mtg_beam_config* cfg, int32_t* out_tokens, int out_stride,
+                     int32_t* out_len, float* out_logprob, float* out_norm_score,
+                     uint32_t* out_flags, int32_t* out_status);
+
 int mtg_forced_logits(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
                       int n_sentences, const int32_t* forced, int n_forced,
                       float* out_logits);

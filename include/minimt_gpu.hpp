@@ -17,7 +17,11 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <fstream>
 #include <functional>
+#include <map>
+#include <set>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -127,9 +131,15 @@ struct BatchResult {
   std::vector<int> status;
 };
 
+// Per sentence: the model's source-factor id streams, each aligned with the
+// sentence's ids (EOS position included).
+using FactorStreams = std::vector<std::vector<std::vector<int>>>;
+
 inline BatchResult translate_ids(const GpuExecutor& ex,
                                  const std::vector<std::vector<int>>& sources,
-                                 const BeamConfig& config, int max_batch = 0) {
+                                 const BeamConfig& config, int max_batch = 0,
+                                 const FactorStreams* factors = nullptr,
+                                 const std::vector<std::vector<int>>* shortlists = nullptr) {
   std::vector<int32_t> ids;
   std::vector<int64_t> off{0};
   for (const auto& s : sources) {
@@ -143,8 +153,38 @@ inline BatchResult translate_ids(const GpuExecutor& ex,
   std::vector<float> lp(std::max(n, 1)), norm(std::max(n, 1));
   std::vector<uint32_t> flags(std::max(n, 1));
   mtg_beam_config c{config.beam_size, config.max_len, config.length_penalty_alpha, max_batch};
-  check(mtg_translate(ex.handle(), ids.data(), off.data(), n, &c, toks.data(), T, len.data(),
-                      lp.data(), norm.data(), flags.data(), status.data()));
+  std::vector<int32_t> block;
+  int nf = 0;
+  if (factors) {  // [F][total] block aligned with ids (minimt_gpu.h)
+    if (static_cast<int>(factors->size()) != n)
+      throw ShapeError("factor streams: one entry per sentence");
+    nf = n ? static_cast<int>((*factors)[0].size()) : 0;
+    block.assign(static_cast<size_t>(std::max(nf, 1)) * std::max<size_t>(ids.size(), 1), 0);
+    for (int i = 0; i < n; ++i) {
+      if (static_cast<int>((*factors)[i].size()) != nf)
+        throw ShapeError("factor streams: every sentence needs the same stream count");
+      for (int f = 0; f < nf; ++f) {
+        const auto& st = (*factors)[i][f];
+        if (static_cast<int64_t>(st.size()) != off[i + 1] - off[i])
+          throw ShapeError("embed_source: factor stream not aligned with words");
+        std::copy(st.begin(), st.end(), block.begin() + f * ids.size() + off[i]);
+      }
+    }
+  }
+  std::vector<int32_t> sl_ids;
+  std::vector<int64_t> sl_off{0};
+  if (shortlists) {  // CSR; an empty list decodes over the full vocabulary
+    if (static_cast<int>(shortlists->size()) != n) throw ShapeError("one shortlist per sentence");
+    for (const auto& l : *shortlists) {
+      sl_ids.insert(sl_ids.end(), l.begin(), l.end());
+      sl_off.push_back(static_cast<int64_t>(sl_ids.size()));
+    }
+    if (sl_ids.empty()) sl_ids.push_back(0);
+  }
+  check(mtg_translate_ex(ex.handle(), ids.data(), off.data(), n, factors ? block.data() : nullptr,
+                         nf, shortlists ? sl_ids.data() : nullptr,
+                         shortlists ? sl_off.data() : nullptr, &c, toks.data(), T, len.data(),
+                         lp.data(), norm.data(), flags.data(), status.data()));
   BatchResult r;
   for (int i = 0; i < n; ++i) {
     Hypothesis h;
@@ -160,18 +200,82 @@ inline BatchResult translate_ids(const GpuExecutor& ex,
   return r;
 }
 
-// decode.hpp:35-38. Factor streams and shortlists are not on the GPU path yet.
+// decode.hpp:35-38.
 inline Hypothesis beam_search(const GpuExecutor& ex, const std::vector<int>& src_ids,
                               const std::vector<std::vector<int>>& factor_ids,
                               const BeamConfig& config,
                               const std::vector<int>* shortlist = nullptr) {
   if (config.beam_size < 1) throw UsageError("beam_search: beam size >= 1");
   if (src_ids.empty()) throw UsageError("beam_search: empty source");
-  if (!factor_ids.empty()) throw UsageError("source factors are not supported on the GPU path");
-  if (shortlist) throw UsageError("shortlists are not supported on the GPU path yet");
-  BatchResult r = translate_ids(ex, {src_ids}, config);
+  const FactorStreams fs{factor_ids};
+  const std::vector<std::vector<int>> sl{shortlist ? *shortlist : std::vector<int>{}};
+  BatchResult r = translate_ids(ex, {src_ids}, config, 0, &fs, shortlist ? &sl : nullptr);
   if (r.status[0] != MTG_OK) throw_status(r.status[0], "beam_search failed");
   return r.hyps[0];
+}
+
+// ---- lexical shortlist (decode.cpp:113-199) --------------------------------------
+// Source id -> target candidates ranked by co-occurrence count (desc, id asc).
+struct ShortlistTable {
+  std::map<int, std::vector<std::pair<int, long>>> candidates;
+
+  void save(const std::string& path) const {  // "s t:c t:c ..." per line
+    std::ofstream f(path, std::ios::trunc);
+    if (!f) throw IoError("cannot write shortlist table: " + path);
+    for (const auto& [s, ranked] : candidates) {
+      f << s;
+      for (const auto& [t, c] : ranked) f << ' ' << t << ':' << c;
+      f << '\n';
+    }
+  }
+  static ShortlistTable load(const std::string& path) {
+    std::ifstream f(path);
+    if (!f) throw IoError("cannot read shortlist table: " + path);
+    ShortlistTable table;
+    std::string line;
+    while (std::getline(f, line)) {
+      if (line.empty()) continue;
+      std::istringstream ss(line);
+      int s;
+      ss >> s;
+      std::string entry;
+      auto& ranked = table.candidates[s];
+      while (ss >> entry) {
+        const auto colon = entry.find(':');
+        if (colon == std::string::npos) throw FormatError("bad shortlist entry: " + entry);
+        ranked.emplace_back(std::stoi(entry.substr(0, colon)), std::stol(entry.substr(colon + 1)));
+      }
+    }
+    return table;
+  }
+};
+
+// Merged candidates of the source ids (best count per target), ranked, plus
+// the four reserved ids, cut at k; sorted ascending. k <= 0 or k >= V: all ids.
+inline std::vector<int> build_shortlist(const ShortlistTable& table, const std::vector<int>& src_ids,
+                                        int k, int tgt_vocab_size) {
+  std::vector<int> out;
+  if (k <= 0 || k >= tgt_vocab_size) {
+    out.resize(tgt_vocab_size);
+    for (int i = 0; i < tgt_vocab_size; ++i) out[i] = i;
+    return out;
+  }
+  std::map<int, long> merged;
+  for (int s : src_ids) {
+    const auto it = table.candidates.find(s);
+    if (it == table.candidates.end()) continue;
+    for (const auto& [t, c] : it->second) merged[t] = std::max(merged[t], c);
+  }
+  std::vector<std::pair<int, long>> ranked(merged.begin(), merged.end());
+  std::sort(ranked.begin(), ranked.end(), [](const auto& a, const auto& b) {
+    return a.second != b.second ? a.second > b.second : a.first < b.first;
+  });
+  std::set<int> result{kPadId, kUnkId, kBosId, kEosId};
+  for (const auto& [t, c] : ranked) {
+    if (static_cast<int>(result.size()) >= k) break;
+    if (t < tgt_vocab_size) result.insert(t);
+  }
+  return std::vector<int>(result.begin(), result.end());
 }
 
 // ---- decode.hpp:81-113 ------------------------------------------------------------

@@ -258,6 +258,39 @@ int orc_encode(void* hv, int int8, const int* src, int n_src, float* out) {
   });
 }
 
+// Source-factor variants: fids holds n_factors streams of n_src ids each
+// (stream f at fids + f * n_src), aligned with src (model.cpp:539-581).
+static std::vector<std::vector<int>> factor_streams(const int* fids, int n_factors, int n_src) {
+  std::vector<std::vector<int>> f;
+  for (int i = 0; i < n_factors; ++i)
+    f.push_back(vec(fids + static_cast<long long>(i) * n_src, n_src));
+  return f;
+}
+
+int orc_encode_factors(void* hv, int int8, const int* src, int n_src, const int* fids,
+                       int n_factors, float* out) {
+  return guard([&] {
+    Handle* h = static_cast<Handle*>(hv);
+    const Executor& ex = h->exec(int8);
+    Tensor enc = encode_infer(
+        ex, embed_source_infer(ex, vec(src, n_src), factor_streams(fids, n_factors, n_src)));
+    std::memcpy(out, enc.data.data(), sizeof(float) * enc.data.size());
+  });
+}
+
+int orc_beam_search_factors(void* hv, int int8, const int* src, int n_src, const int* fids,
+                            int n_factors, int beam, int max_len, float alpha, int* out_tokens,
+                            int cap, int* out_len, float* out_lp, float* out_norm,
+                            int* out_flags) {
+  return guard([&] {
+    Handle* h = static_cast<Handle*>(hv);
+    BeamConfig cfg{beam, max_len, alpha};
+    Hypothesis hyp = beam_search(h->exec(int8), vec(src, n_src),
+                                 factor_streams(fids, n_factors, n_src), cfg, nullptr);
+    write_hyp(hyp, alpha, out_tokens, cap, out_len, out_lp, out_norm, out_flags);
+  });
+}
+
 int orc_quantize(const float* x, long long n, int8_t* q, float* scale) {
   return guard([&] {
     QTensor t = quantize(x, {n});

@@ -105,6 +105,14 @@ def _load():
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.mtg_forced_logits.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p]
     lib.mtg_encode.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_void_p]
+    lib.mtg_translate_factors.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int,
+                                          c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p]
+    lib.mtg_encode_factors.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int,
+                                       c_void_p]
+    lib.mtg_translate_ex.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p,
+                                     c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                     c_void_p, c_void_p, c_void_p]
     lib.mtg_stage_sources.argtypes = [c_void_p, c_void_p, c_void_p, c_int]
     lib.mtg_translate_staged.argtypes = [c_void_p, c_void_p]
     lib.mtg_last_launch_count.argtypes = [c_void_p]
@@ -235,6 +243,20 @@ def gemm(a: np.ndarray, b: np.ndarray, precision: int = F32) -> np.ndarray:
     return c
 
 
+def _factor_block(factors, off, n_factors: int):
+    """[n_factors][total] ids aligned with the CSR source ids (minimt_gpu.h)."""
+    total = int(off[-1])
+    out = np.zeros((max(n_factors, 1), max(total, 1)), np.int32)
+    for i, streams in enumerate(factors):
+        if len(streams) != n_factors:
+            raise ShapeError("factor streams: every sentence needs the same stream count")
+        for f, stream in enumerate(streams):
+            if len(stream) != off[i + 1] - off[i]:
+                raise ShapeError("embed_source: factor stream not aligned with words")
+            out[f, off[i]:off[i + 1]] = np.asarray(stream, np.int32)
+    return out
+
+
 def _csr(sources: Sequence[Sequence[int]]):
     off = np.zeros(len(sources) + 1, np.int64)
     for i, s in enumerate(sources):
@@ -293,9 +315,13 @@ class Model:
         return int(self.config["max_seq_len"])
 
     def translate(self, sources: Sequence[Sequence[int]], cfg: BeamConfig,
-                  max_batch: int = 0) -> List[Hypothesis]:
+                  max_batch: int = 0, factors=None, shortlists=None) -> List[Hypothesis]:
         """Batched beam_search (decode.cpp:34-109) over id sequences that already
-        end with EOS. Per-sentence errors come back in Hypothesis.status."""
+        end with EOS. Per-sentence errors come back in Hypothesis.status.
+        factors: per sentence, the model's source-factor streams (each aligned
+        with its source, EOS position included). shortlists: per sentence a
+        strictly increasing target-id list, or an empty one for the full
+        vocabulary (decode.cpp:344-349)."""
         ids, off = _csr(sources)
         n = len(sources)
         T = self.max_seq_len
@@ -306,8 +332,23 @@ class Model:
         fl = np.zeros(max(n, 1), np.uint32)
         st = np.zeros(max(n, 1), np.int32)
         c = _BeamConfigC(cfg.beam_size, cfg.max_len, cfg.length_penalty_alpha, max_batch)
-        _check(_lib.mtg_translate(self._h, _ptr(ids), _ptr(off), n, ctypes.byref(c), _ptr(toks), T,
-                                  _ptr(ln), _ptr(lp), _ptr(nm), _ptr(fl), _ptr(st)))
+        if shortlists is not None:
+            nf = len(factors[0]) if (factors is not None and n) else 0
+            fb = _factor_block(factors, off, nf) if factors is not None else None
+            sl_ids, sl_off = _csr(shortlists)
+            _check(_lib.mtg_translate_ex(self._h, _ptr(ids), _ptr(off), n,
+                                         None if fb is None else _ptr(fb), nf, _ptr(sl_ids),
+                                         _ptr(sl_off), ctypes.byref(c), _ptr(toks), T, _ptr(ln),
+                                         _ptr(lp), _ptr(nm), _ptr(fl), _ptr(st)))
+        elif factors is not None:
+            nf = len(factors[0]) if n else 0
+            fb = _factor_block(factors, off, nf)
+            _check(_lib.mtg_translate_factors(self._h, _ptr(ids), _ptr(off), n, _ptr(fb), nf,
+                                              ctypes.byref(c), _ptr(toks), T, _ptr(ln), _ptr(lp),
+                                              _ptr(nm), _ptr(fl), _ptr(st)))
+        else:
+            _check(_lib.mtg_translate(self._h, _ptr(ids), _ptr(off), n, ctypes.byref(c), _ptr(toks),
+                                      T, _ptr(ln), _ptr(lp), _ptr(nm), _ptr(fl), _ptr(st)))
         return [Hypothesis(toks[i, :ln[i]].tolist(), float(lp[i]), bool(fl[i] & HYP_FINISHED),
                            bool(fl[i] & HYP_TRUNCATED), float(nm[i]), int(st[i])) for i in range(n)]
 
@@ -321,11 +362,17 @@ class Model:
                                       _ptr(out)))
         return out
 
-    def encode(self, sources: Sequence[Sequence[int]]) -> np.ndarray:
+    def encode(self, sources: Sequence[Sequence[int]], factors=None) -> np.ndarray:
         """encode_infer(embed_source_infer(.)) rows, concatenated."""
         ids, off = _csr(sources)
         out = np.zeros((int(off[-1]), int(self.config["d_model"])), np.float32)
-        _check(_lib.mtg_encode(self._h, _ptr(ids), _ptr(off), len(sources), _ptr(out)))
+        if factors is not None:
+            nf = len(factors[0]) if len(sources) else 0
+            fb = _factor_block(factors, off, nf)
+            _check(_lib.mtg_encode_factors(self._h, _ptr(ids), _ptr(off), len(sources), _ptr(fb),
+                                           nf, _ptr(out)))
+        else:
+            _check(_lib.mtg_encode(self._h, _ptr(ids), _ptr(off), len(sources), _ptr(out)))
         return out
 
     # benchmark helpers: device-resident sources
@@ -349,17 +396,16 @@ class Model:
 
 def beam_search(model: Model, src_ids: Sequence[int], factor_ids=(), config: BeamConfig = None,
                 shortlist=None) -> Hypothesis:
-    """decode.hpp:35-38 for one sentence (factors/shortlist: not yet on GPU)."""
-    if factor_ids:
-        raise UsageError("source factors are not supported by the GPU path yet")
-    if shortlist is not None:
-        raise UsageError("shortlists are not supported by the GPU path yet")
+    """decode.hpp:35-38 for one sentence."""
     cfg = config or BeamConfig()
     if cfg.beam_size < 1:
         raise UsageError("beam_search: beam size >= 1")
     if len(src_ids) == 0:
         raise UsageError("beam_search: empty source")
-    h = model.translate([list(src_ids)], cfg)[0]
+    n_f = len(model.config.get("factors", []) or [])
+    fac = [[list(f) for f in factor_ids]] if (factor_ids or n_f) else None
+    sl = [list(shortlist)] if shortlist is not None else None
+    h = model.translate([list(src_ids)], cfg, factors=fac, shortlists=sl)[0]
     if h.status:
         raise _ERRORS.get(h.status, MinimtError)("beam_search failed")
     return h

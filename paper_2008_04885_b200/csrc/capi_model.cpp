@@ -77,10 +77,28 @@ int mtg_model_config_json(const mtg_model* m, char* buf, size_t cap) {
 
 int mtg_model_precision(const mtg_model* m) { return m && m->eng ? m->eng->precision() : -1; }
 
-int mtg_translate(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
-                  int n_sentences, const mtg_beam_config* cfg, int32_t* out_tokens,
-                  int out_stride, int32_t* out_len, float* out_logprob, float* out_norm_score,
-                  uint32_t* out_flags, int32_t* out_status) {
+}  // extern "C"
+
+namespace {
+
+// Factor streams of sentence s: stream f is factor_ids[f * total + off[s] ..).
+Engine::FactorStreams factor_streams(const int32_t* factor_ids, int n_factors,
+                                     const int64_t* off, int n) {
+  Engine::FactorStreams fs(n);
+  if (!factor_ids || n_factors <= 0) return fs;
+  const int64_t total = off[n];
+  for (int s = 0; s < n; ++s)
+    for (int f = 0; f < n_factors; ++f)
+      fs[s].emplace_back(factor_ids + f * total + off[s], factor_ids + f * total + off[s + 1]);
+  return fs;
+}
+
+int translate_impl(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                   int n_sentences, const int32_t* factor_ids, int n_factors,
+                   const int32_t* sl_ids, const int64_t* sl_offsets,
+                   const mtg_beam_config* cfg, int32_t* out_tokens, int out_stride,
+                   int32_t* out_len, float* out_logprob, float* out_norm_score,
+                   uint32_t* out_flags, int32_t* out_status) {
   return guarded([&] {
     Engine& e = engine(m);
     std::lock_guard<std::mutex> lock(e.mutex());
@@ -89,6 +107,9 @@ int mtg_translate(mtg_model* m, const int32_t* src_ids, const int64_t* src_offse
     if (out_tokens && out_stride < e.config().max_seq_len)
       fail(kShapeError, "out_stride must be >= max_seq_len");
     auto srcs = csr(src_ids, src_offsets, n_sentences);
+    const bool has_f = factor_ids && n_factors > 0;
+    const Engine::FactorStreams all_f =
+        factor_streams(factor_ids, n_factors, src_offsets, n_sentences);
     BeamConfigC bc{cfg->beam_size, cfg->max_len, cfg->length_penalty_alpha};
     // Length-bucketed batching: stable sort by source length so a
     // device batch runs for about as many steps as each of its sentences.
@@ -97,11 +118,27 @@ int mtg_translate(mtg_model* m, const int32_t* src_ids, const int64_t* src_offse
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return srcs[a].size() < srcs[b].size(); });
     const int per = cfg->max_batch > 0 ? cfg->max_batch : std::max(n_sentences, 1);
-    for (int b0 = 0; b0 < n_sentences; b0 += per) {
-      const int b1 = std::min(n_sentences, b0 + per);
-      std::vector<std::vector<int>> chunk;
-      for (int i = b0; i < b1; ++i) chunk.push_back(srcs[order[i]]);
-      std::vector<SentenceResult> res = e.translate_batch(chunk, bc);
+    // Sentences with a shortlist (non-empty CSR entry) and without one run
+    // as separate device batches (the projection differs).
+    auto has_sl = [&](int s) { return sl_ids && sl_offsets && sl_offsets[s + 1] > sl_offsets[s]; };
+    std::stable_partition(order.begin(), order.end(), [&](int s) { return !has_sl(s); });
+    const int n_plain = static_cast<int>(
+        std::count_if(order.begin(), order.end(), [&](int s) { return !has_sl(s); }));
+    std::vector<std::pair<int, int>> chunks;
+    for (int b0 = 0; b0 < n_plain; b0 += per) chunks.push_back({b0, std::min(n_plain, b0 + per)});
+    for (int b0 = n_plain; b0 < n_sentences; b0 += per)
+      chunks.push_back({b0, std::min(n_sentences, b0 + per)});
+    for (const auto& [b0, b1] : chunks) {
+      std::vector<std::vector<int>> chunk, chunk_sl;
+      Engine::FactorStreams chunk_f;
+      for (int i = b0; i < b1; ++i) {
+        chunk.push_back(srcs[order[i]]);
+        if (has_f) chunk_f.push_back(all_f[order[i]]);
+        if (b0 >= n_plain)
+          chunk_sl.emplace_back(sl_ids + sl_offsets[order[i]], sl_ids + sl_offsets[order[i] + 1]);
+      }
+      std::vector<SentenceResult> res = e.translate_batch(
+          chunk, bc, has_f ? &chunk_f : nullptr, b0 >= n_plain ? &chunk_sl : nullptr);
       for (int i = b0; i < b1; ++i) {
         const int s = order[i];
         const SentenceResult& r = res[i - b0];
@@ -115,6 +152,52 @@ int mtg_translate(mtg_model* m, const int32_t* src_ids, const int64_t* src_offse
         if (out_status) out_status[s] = r.status;
       }
     }
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int mtg_translate(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                  int n_sentences, const mtg_beam_config* cfg, int32_t* out_tokens,
+                  int out_stride, int32_t* out_len, float* out_logprob, float* out_norm_score,
+                  uint32_t* out_flags, int32_t* out_status) {
+  return translate_impl(m, src_ids, src_offsets, n_sentences, nullptr, 0, nullptr, nullptr, cfg,
+                        out_tokens, out_stride, out_len, out_logprob, out_norm_score, out_flags,
+                        out_status);
+}
+
+int mtg_translate_factors(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                          int n_sentences, const int32_t* factor_ids, int n_factors,
+                          const mtg_beam_config* cfg, int32_t* out_tokens, int out_stride,
+                          int32_t* out_len, float* out_logprob, float* out_norm_score,
+                          uint32_t* out_flags, int32_t* out_status) {
+  return translate_impl(m, src_ids, src_offsets, n_sentences, factor_ids, n_factors, nullptr,
+                        nullptr, cfg, out_tokens, out_stride, out_len, out_logprob,
+                        out_norm_score, out_flags, out_status);
+}
+
+int mtg_translate_ex(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                     int n_sentences, const int32_t* factor_ids, int n_factors,
+                     const int32_t* shortlist_ids, const int64_t* shortlist_offsets,
+                     const mtg_beam_config* cfg, int32_t* out_tokens, int out_stride,
+                     int32_t* out_len, float* out_logprob, float* out_norm_score,
+                     uint32_t* out_flags, int32_t* out_status) {
+  return translate_impl(m, src_ids, src_offsets, n_sentences, factor_ids, n_factors,
+                        shortlist_ids, shortlist_offsets, cfg, out_tokens, out_stride, out_len,
+                        out_logprob, out_norm_score, out_flags, out_status);
+}
+
+int mtg_encode_factors(mtg_model* m, const int32_t* src_ids, const int64_t* src_offsets,
+                       int n_sentences, const int32_t* factor_ids, int n_factors, float* out) {
+  return guarded([&] {
+    Engine& e = engine(m);
+    std::lock_guard<std::mutex> lock(e.mutex());
+    const Engine::FactorStreams fs =
+        factor_streams(factor_ids, n_factors, src_offsets, n_sentences);
+    e.encode(csr(src_ids, src_offsets, n_sentences), out,
+             factor_ids && n_factors > 0 ? &fs : nullptr);
   });
 }
 

@@ -161,8 +161,8 @@ Engine::Engine(HostModel model, int precision, int device)
   if (prec_ == kINT8 && !host_.quantized) quantize_weights(host_);
   const ModelConfig& c = host_.config;
   c.validate();
-  if (!c.factor_configs.empty())
-    fail(kUsageError, "source factors are not supported by the GPU path yet");
+  if (static_cast<int>(c.factor_configs.size()) > kMaxFactors)
+    fail(kUsageError, "at most 4 source factors are supported by the GPU path");
   int ndev = 0;
   MTG_CUDA(cudaGetDeviceCount(&ndev));
   if (device_ < 0 || device_ >= ndev) fail(kUsageError, "bad device id " + std::to_string(device_));
@@ -193,6 +193,11 @@ void Engine::upload_weights() {
   const ModelConfig& c = host_.config;
   auto P = [&](const std::string& n) -> const HostTensor& { return host_.at(n); };
   upload_vec(src_embed_, P("src_embed"));
+  factor_embed_.clear();
+  factor_embed_.resize(c.factor_configs.size());
+  for (size_t i = 0; i < c.factor_configs.size(); ++i)
+    if (!c.factor_configs[i].share_with_word_embedding)
+      upload_vec(factor_embed_[i], P("factor" + std::to_string(i) + "_embed"));
   std::vector<float> pe = make_pos_enc(c.max_seq_len, c.d_model);
   pe_.resize(pe.size());
   pe_.upload(pe.data(), pe.size(), stream_);
@@ -494,6 +499,32 @@ std::string Engine::diag_report() const {
   return out;
 }
 
+ShortlistArgs Engine::shortlist_args() const {
+  ShortlistArgs a;
+  a.sl_ids = sl_ids_.get();
+  a.sl_off = sl_off_.get();
+  a.K = d_;
+  if (prec_ == kINT8) {
+    a.aq = act_d_.q.get();
+    a.a_scale = act_d_.row_scale.get();
+    a.lda = act_d_.k_pad;
+    a.wq = logits_w_.q.get();
+    a.ldw = logits_w_.k_pad;
+    a.w_scale = tgt_scale_;
+  } else if (prec_ == kBF16) {
+    a.ah = act_d_.h.get();
+    a.lda = act_d_.k_pad;
+    a.wh = logits_w_.h.get();
+    a.ldw = logits_w_.k_pad;
+  } else {
+    a.af = dec_a_.get();
+    a.lda = d_;
+    a.wf = tgt_embed_f32_.get();
+    a.ldw = d_;
+  }
+  return a;
+}
+
 void Engine::gemm_logits(int m, const int* d_m) {
   auto& cache = plan_cache(this);
   PlanKey key{act_d_.op().ptr, logits_w_.op().ptr, m};
@@ -534,17 +565,36 @@ void Engine::gemm_logits(int m, const int* d_m) {
 int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status) {
   const int n = static_cast<int>(srcs.size());
   const ModelConfig& c = host_.config;
+  const int nf = static_cast<int>(c.factor_configs.size());
+  const auto* fac = staged_factors_.empty() ? nullptr : &staged_factors_;
   status.assign(n, 0);
   std::vector<int> ids, pos, seg, off(n + 1, 0), eoff(n, 0), elen(n, 0);
+  std::vector<std::vector<int>> fids(nf);
   for (int s = 0; s < n; ++s) {
     const auto& src = srcs[s];
-    if (src.empty())
+    // beam_search (decode.cpp:38-39), then embed_source_infer's checks in
+    // order (model.cpp:541-548, tensor.cpp:456-458).
+    const int have = fac ? static_cast<int>((*fac)[s].size()) : 0;
+    if (src.empty()) {
       status[s] = kUsageError;
-    else if (static_cast<int>(src.size()) > c.max_seq_len)
-      status[s] = kValueError;
-    else
-      for (int id : src)
-        if (id < 0 || id >= c.src_vocab_size) status[s] = kIndexError;
+    } else if (have != nf) {
+      status[s] = kShapeError;
+    } else {
+      for (int f = 0; f < nf; ++f)
+        if ((*fac)[s][f].size() != src.size()) status[s] = kShapeError;
+      if (status[s] == 0 && static_cast<int>(src.size()) > c.max_seq_len) status[s] = kValueError;
+      if (status[s] == 0)
+        for (int id : src)
+          if (id < 0 || id >= c.src_vocab_size) status[s] = kIndexError;
+      for (int f = 0; f < nf && status[s] == 0; ++f) {
+        const int rows = c.factor_configs[f].share_with_word_embedding
+                             ? c.src_vocab_size
+                             : c.factor_configs[f].factor_vocab_size;
+        for (int id : (*fac)[s][f])
+          if (id < 0 || id >= rows) status[s] = kIndexError;
+      }
+    }
+    if (status[s] == 0 && s < static_cast<int>(sl_status_.size())) status[s] = sl_status_[s];
     off[s] = static_cast<int>(ids.size());
     eoff[s] = off[s];
     if (status[s] == 0) {
@@ -552,6 +602,7 @@ int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector
         ids.push_back(src[i]);
         pos.push_back(static_cast<int>(i));
         seg.push_back(s);
+        for (int f = 0; f < nf; ++f) fids[f].push_back((*fac)[s][f][i]);
       }
       elen[s] = static_cast<int>(src.size());
     }
@@ -562,6 +613,11 @@ int Engine::stage_sources(const std::vector<std::vector<int>>& srcs, std::vector
     src_ids_.upload(ids.data(), m, stream_);
     src_pos_.upload(pos.data(), m, stream_);
     src_rowseg_.upload(seg.data(), m, stream_);
+    if (nf > 0) {
+      src_fids_.resize(static_cast<size_t>(nf) * m);
+      for (int f = 0; f < nf; ++f) src_fids_.upload(fids[f].data(), m, stream_, size_t(f) * m);
+      MTG_CUDA(cudaStreamSynchronize(stream_));  // host vectors are freed on return
+    }
   }
   src_off_.upload(off.data(), n + 1, stream_);
   enc_off_.upload(eoff.data(), n, stream_);
@@ -650,8 +706,24 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
   const long long d = d_;
   const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
   const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
-  launch_embed_src(src_ids_.get(), src_pos_.get(), m, src_embed_.get(), d_, sqrt_d, pe_.get(),
-                   enc_x_.get(), d, stream_);
+  SrcEmbed se;
+  se.word = src_embed_.get();
+  se.wdim = c.word_embed_dim();
+  se.n_factors = static_cast<int>(c.factor_configs.size());
+  if (se.n_factors > 0) {
+    const FactorCombine mode = c.factor_configs.front().combine;
+    se.mode = mode == FactorCombine::kConcat ? 0 : mode == FactorCombine::kSum ? 1 : 2;
+    for (int f = 0; f < se.n_factors; ++f) {
+      se.table[f] = c.factor_configs[f].share_with_word_embedding ? src_embed_.get()
+                                                                  : factor_embed_[f].get();
+      se.fdim[f] = c.factor_configs[f].embed_dim;
+    }
+    se.fids = src_fids_.get();
+    se.fstride = m;
+    se.avg_scale = 1.0f / (1.0f + static_cast<float>(se.n_factors));  // model.cpp:573
+  }
+  launch_embed_src(src_ids_.get(), src_pos_.get(), m, se, d_, sqrt_d, pe_.get(), enc_x_.get(), d,
+                   stream_);
   count("enc embed");
   enc_n_sent_ = n_sent;
   // int8 with d <= 512: the LayerNorms quantize per sentence themselves and
@@ -721,11 +793,13 @@ void Engine::decoder_body(bool reorder) {
   // Executor::linear call in decode_step), so LayerNorm and attention write
   // the next GEMM's operand directly.
   const OperandOut od = opout(act_d_);
-  auto ln_dec = [&](const LN& ln) {
-    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), nullptr, d, nullptr,
-                     &od, stream_);
+  auto ln_dec = [&](const LN& ln, float* y = nullptr) {
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), y, d, nullptr, &od,
+                     stream_);
     count("layernorm");
   };
+  // Shortlist decoding reads the final LayerNorm rows themselves (fp32 path).
+  float* final_y = use_shortlist_ ? dec_a_.get() : nullptr;
   // Step start: history reorder + target embedding + first LayerNorm fused
   // into one kernel (d_model <= 512), else three kernels.
   // MTG_STEP_FUSION: 0 = three kernels, 1 = reorder + fused embed/LN,
@@ -734,7 +808,7 @@ void Engine::decoder_body(bool reorder) {
     const char* e = std::getenv("MTG_STEP_FUSION");
     return e ? std::atoi(e) : 0;
   }();
-  const bool fused = d_ <= 512 && fusion > 0;
+  const bool fused = d_ <= 512 && fusion > 0 && !(use_shortlist_ && c.num_decoder_layers == 0);
   const LN& ln0 = c.num_decoder_layers > 0 ? dec_[0].n1 : dec_final_;
   if (fused) {
     StepBegin sb{};
@@ -771,7 +845,7 @@ void Engine::decoder_body(bool reorder) {
                      tgt_scale_, d_, sqrt_d,
                      pe_.get(), dec_y_.get(), d, stream_);
     count("embed_tgt");
-    ln_dec(ln0);
+    ln_dec(ln0, c.num_decoder_layers == 0 ? final_y : nullptr);
   }
   for (int l = 0; l < c.num_decoder_layers; ++l) {
     DecLayer& L = dec_[l];
@@ -794,8 +868,8 @@ void Engine::decoder_body(bool reorder) {
     prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
     gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
   }
-  if (c.num_decoder_layers > 0) ln_dec(dec_final_);
-  gemm_logits(R, dr);
+  if (c.num_decoder_layers > 0) ln_dec(dec_final_, final_y);
+  if (!use_shortlist_) gemm_logits(R, dr);  // shortlists project inside their top-k kernel
 }
 
 void Engine::ensure_step_graph() {
@@ -805,6 +879,9 @@ void Engine::ensure_step_graph() {
   key.r_max = r_max_;
   key.gen = ws_gen_;
   key.alpha = beam_.alpha;
+  key.shortlist = use_shortlist_;
+  key.sl_ids = sl_ids_.get();
+  key.sl_off = sl_off_.get();
   if (step_exec_ && key == step_key_) return;
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);
@@ -821,9 +898,15 @@ void Engine::ensure_step_graph() {
       MTG_CUDA(cudaEventRecordWithFlags(diag_marks_.back().ev, stream_, cudaEventRecordExternal));
     }
     decoder_body(true);
-    launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
-                        part_ld_, beam_, stream_);
-    count("softmax + top-k merge");
+    if (use_shortlist_) {
+      launch_shortlist_topk(prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2, shortlist_args(), beam_,
+                            stream_);
+      count("shortlist logits + softmax + top-k");
+    } else {
+      launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
+                          part_ld_, beam_, stream_);
+      count("softmax + top-k merge");
+    }
     launch_beam_select(beam_, stream_);
     count("beam select");
   } catch (...) {
@@ -872,8 +955,10 @@ void Engine::decode_loop(int t_run) {
 // ============================================================================
 
 std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vector<int>>& srcs,
-                                                    const BeamConfigC& cfg) {
-  stage(srcs);
+                                                    const BeamConfigC& cfg,
+                                                    const FactorStreams* factors,
+                                                    const std::vector<std::vector<int>>* shortlists) {
+  stage(srcs, factors, shortlists);
   run_staged(cfg);
   const int n = staged_n_;
   std::vector<SentenceResult> out(n);
@@ -907,8 +992,40 @@ std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vecto
   return out;
 }
 
-void Engine::stage(const std::vector<std::vector<int>>& srcs) {
+void Engine::stage(const std::vector<std::vector<int>>& srcs, const FactorStreams* factors,
+                   const std::vector<std::vector<int>>* shortlists) {
   const int n = static_cast<int>(srcs.size());
+  if (factors && static_cast<int>(factors->size()) != n)
+    fail(kShapeError, "factor streams: one entry per sentence");
+  staged_factors_ = factors ? *factors : FactorStreams{};
+  // Shortlists (decode.cpp:344-349): all or none of a device batch; ids must
+  // be valid target rows (IndexError, model.cpp:446) in increasing order.
+  use_shortlist_ = false;
+  sl_status_.clear();
+  if (shortlists) {
+    if (static_cast<int>(shortlists->size()) != n) fail(kShapeError, "one shortlist per sentence");
+    std::vector<int> ids, off(n + 1, 0);
+    sl_status_.assign(n, 0);
+    for (int s = 0; s < n; ++s) {
+      const auto& l = (*shortlists)[s];
+      if (l.empty()) fail(kStateError, "shortlist batch mixes sentences without a shortlist");
+      // Per-sentence failures (the reference throws from the first
+      // decode_step, after source validation).
+      if (static_cast<int>(l.size()) > kMaxShortlist) sl_status_[s] = kUsageError;
+      for (size_t j = 0; j < l.size() && !sl_status_[s]; ++j) {
+        if (l[j] < 0 || l[j] >= V_) sl_status_[s] = kIndexError;  // model.cpp:446
+        else if (j > 0 && l[j] <= l[j - 1]) sl_status_[s] = kUsageError;  // must be sorted
+      }
+      if (!sl_status_[s]) ids.insert(ids.end(), l.begin(), l.end());
+      off[s + 1] = static_cast<int>(ids.size());
+    }
+    sl_ids_.resize(std::max<size_t>(ids.size(), 1));
+    sl_off_.resize(n + 1);
+    sl_ids_.upload(ids.data(), ids.size(), stream_);
+    sl_off_.upload(off.data(), n + 1, stream_);
+    MTG_CUDA(cudaStreamSynchronize(stream_));
+    use_shortlist_ = true;
+  }
   int m = 0, max_src = 0;
   for (const auto& s : srcs) {
     if (static_cast<int>(s.size()) <= host_.config.max_seq_len) m += static_cast<int>(s.size());
@@ -1023,10 +1140,10 @@ void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double
 }
 
 void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int* forced, int nf,
-                           float* out) {
+                           float* out, const FactorStreams* factors) {
   const int n = static_cast<int>(srcs.size());
   if (n == 0 || nf <= 0) return;
-  stage(srcs);
+  stage(srcs, factors);
   for (int s = 0; s < n; ++s)
     if (staged_status_[s]) fail(static_cast<Status>(staged_status_[s]), "bad source sentence");
   if (nf > host_.config.max_seq_len) fail(kValueError, "decode_step: past max_seq_len");
@@ -1064,10 +1181,11 @@ void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int*
   last_launches_ = launches_;
 }
 
-void Engine::encode(const std::vector<std::vector<int>>& srcs, float* out) {
+void Engine::encode(const std::vector<std::vector<int>>& srcs, float* out,
+                    const FactorStreams* factors) {
   const int n = static_cast<int>(srcs.size());
   if (n == 0) return;
-  stage(srcs);
+  stage(srcs, factors);
   for (int s = 0; s < n; ++s)
     if (staged_status_[s]) fail(static_cast<Status>(staged_status_[s]), "bad source sentence");
   MTG_CUDA(cudaMemsetAsync(nonfinite_.get(), 0, sizeof(int), stream_));

@@ -71,17 +71,27 @@ class Engine {
   const HostModel& host_model() const { return host_; }
   std::mutex& mutex() { return mu_; }
 
+  // Per sentence: the model's source-factor streams, each aligned with the
+  // source ids (model.cpp:539-546).
+  using FactorStreams = std::vector<std::vector<std::vector<int>>>;
+
   // Batched beam search over one device batch (sources carry their EOS).
-  std::vector<SentenceResult> translate_batch(const std::vector<std::vector<int>>& srcs,
-                                              const BeamConfigC& cfg);
+  // shortlists: per sentence a strictly increasing target-id list (all
+  // sentences of the batch, or null for full-vocabulary decoding).
+  std::vector<SentenceResult> translate_batch(
+      const std::vector<std::vector<int>>& srcs, const BeamConfigC& cfg,
+      const FactorStreams* factors = nullptr,
+      const std::vector<std::vector<int>>* shortlists = nullptr);
   // decode_step logits along forced prefixes; out[(i*nf + t)*V + v].
   void forced_logits(const std::vector<std::vector<int>>& srcs, const int* forced, int nf,
-                     float* out);
+                     float* out, const FactorStreams* factors = nullptr);
   // encode_infer(embed_source_infer(.)) rows.
-  void encode(const std::vector<std::vector<int>>& srcs, float* out);
+  void encode(const std::vector<std::vector<int>>& srcs, float* out,
+              const FactorStreams* factors = nullptr);
 
   // Benchmark support: keep a staged batch resident and re-run it.
-  void stage(const std::vector<std::vector<int>>& srcs);
+  void stage(const std::vector<std::vector<int>>& srcs, const FactorStreams* factors = nullptr,
+             const std::vector<std::vector<int>>* shortlists = nullptr);
   void run_staged(const BeamConfigC& cfg);
   int64_t last_launches() const { return last_launches_; }
   std::string diag_report() const;  // per-kernel step times (MTG_DIAG_EVENTS=1)
@@ -168,7 +178,14 @@ class Engine {
   DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;
   DeviceBuffer<float> part_m_, part_s_;  // [r_max x part_ld_] softmax partials
   DeviceBuffer<int> part_arg_;
-  DeviceBuffer<unsigned> sent_absmax_;  // per-sentence max |x| (float bits), encoder int8
+  DeviceBuffer<unsigned> sent_absmax_;
+  std::vector<DeviceBuffer<float>> factor_embed_;  // non-shared factor tables
+  DeviceBuffer<int> src_fids_;                     // [F][M] staged factor ids
+  FactorStreams staged_factors_;
+  DeviceBuffer<int> sl_ids_, sl_off_;  // shortlist CSR of the staged batch
+  bool use_shortlist_ = false;
+  std::vector<int> sl_status_;  // per staged sentence: shortlist validation status
+  ShortlistArgs shortlist_args() const;  // per-sentence max |x| (float bits), encoder int8
   int enc_n_sent_ = 0;
   bool enc_fused_ = false;
   bool split_k_ = true;
@@ -203,8 +220,12 @@ class Engine {
   struct StepKey {
     int n = -1, b = -1, r_max = -1, gen = -1;
     float alpha = 0.0f;
+    bool shortlist = false;
+    const void* sl_ids = nullptr;  // graph kernels capture these pointers
+    const void* sl_off = nullptr;
     bool operator==(const StepKey& o) const {
-      return n == o.n && b == o.b && r_max == o.r_max && gen == o.gen && alpha == o.alpha;
+      return n == o.n && b == o.b && r_max == o.r_max && gen == o.gen && alpha == o.alpha &&
+             shortlist == o.shortlist && sl_ids == o.sl_ids && sl_off == o.sl_off;
     }
   } step_key_;
 };

@@ -56,16 +56,35 @@ __device__ __forceinline__ void write_operand(const OperandOut& o, long long r, 
 // ---- embeddings -------------------------------------------------------------------
 
 __global__ void embed_src_kernel(const int* __restrict__ ids, const int* __restrict__ pos,
-                                 const float* __restrict__ table, int d, float sqrt_d,
-                                 const float* __restrict__ pe, float* __restrict__ out,
-                                 long long ldo) {
+                                 SrcEmbed se, int d, float sqrt_d, const float* __restrict__ pe,
+                                 float* __restrict__ out, long long ldo) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
-  const float* e = table + static_cast<long long>(ids[r]) * d;
+  const float* w = se.word + static_cast<long long>(ids[r]) * se.wdim;
   const float* p = pe + static_cast<long long>(pos[r]) * d;
   float* o = out + r * ldo;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = __fadd_rn(__fmul_rn(e[c], sqrt_d), p[c]);
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float e;
+    if (se.n_factors == 0) {
+      e = w[c];
+    } else if (se.mode == 0) {  // concat_cols(word, f0, f1, ...)
+      if (c < se.wdim) {
+        e = w[c];
+      } else {
+        int cc = c - se.wdim, f = 0;
+        while (f + 1 < se.n_factors && cc >= se.fdim[f]) cc -= se.fdim[f++];
+        e = se.table[f][static_cast<long long>(se.fids[f * se.fstride + r]) * se.fdim[f] + cc];
+      }
+    } else {  // add(word, f0), add(., f1), ...; average scales by 1/(1+F)
+      e = w[c];
+      for (int f = 0; f < se.n_factors; ++f)
+        e = __fadd_rn(e, se.table[f][static_cast<long long>(se.fids[f * se.fstride + r]) *
+                                         se.fdim[f] + c]);
+      if (se.mode == 2) e = __fmul_rn(e, se.avg_scale);
+    }
+    o[c] = __fadd_rn(__fmul_rn(e, sqrt_d), p[c]);
+  }
 }
 
 __global__ void embed_tgt_kernel(const int* __restrict__ prev, const int* d_rows,
@@ -868,10 +887,11 @@ void set_smem_limit(const void* fn, size_t bytes, const char* what) {
 }
 }  // namespace
 
-void launch_embed_src(const int* ids, const int* pos, int rows, const float* table, int d,
+void launch_embed_src(const int* ids, const int* pos, int rows, const SrcEmbed& se, int d,
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st) {
   if (rows <= 0) return;
-  launch_k(embed_src_kernel, rows, 128, 0, st, ids, pos, table, d, sqrt_d, pe, out, ldo);
+  if (se.n_factors > kMaxFactors) fail(kUsageError, "at most 4 source factors are supported");
+  launch_k(embed_src_kernel, rows, 128, 0, st, ids, pos, se, d, sqrt_d, pe, out, ldo);
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -28,9 +28,23 @@ struct OperandOut {
 // ---- embeddings (model.cpp:539-581, 624-626) -----------------------------------
 
 // out[r] = table[ids[r]] * sqrt_d + pe[pos[r]]
-void launch_embed_src(const int* ids, const int* pos, int rows, const float* table, int d,
-                      float sqrt_d, const float* pe, float* out, long long ldo,
-                      cudaStream_t st);
+// Source embedding (model.cpp:539-581): word row (width wdim) combined with up
+// to kMaxFactors factor rows -- concat (columns appended), sum, or average
+// (sum x 1/(1+F)) -- then x sqrt(d) + PE[pos].
+constexpr int kMaxFactors = 4;
+struct SrcEmbed {
+  const float* word = nullptr;
+  int wdim = 0;
+  int n_factors = 0;
+  int mode = 0;  // 0 concat, 1 sum, 2 average
+  const float* table[kMaxFactors] = {};
+  int fdim[kMaxFactors] = {};
+  const int* fids = nullptr;  // [n_factors][rows]
+  long long fstride = 0;
+  float avg_scale = 1.0f;
+};
+void launch_embed_src(const int* ids, const int* pos, int rows, const SrcEmbed& se, int d,
+                      float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st);
 
 // Decoder input rows (d_rows on device), position = *d_step. table_q != null:
 // int8 table dequantised as q / scale (model.cpp:485).
@@ -159,6 +173,25 @@ void launch_beam_init(const BeamDev& b, cudaStream_t st);
 constexpr int kMaxSoftmaxSlices = 1024;
 long long topk_pitch(int V);          // logits row pitch (elements)
 long long softmax_part_pitch(int V);  // partials row pitch (slices, multiple of 4)
+// Vocabulary shortlist path (topk.cu shortlist_topk_kernel): per-sentence
+// sorted id lists in CSR; operand row r of the final LayerNorm output and the
+// tied output embedding in the path's precision (0 int8, 1 bf16, 2 fp32).
+constexpr int kMaxShortlist = 4096;
+struct ShortlistArgs {
+  const int* sl_ids = nullptr;
+  const int* sl_off = nullptr;  // [N + 1]
+  int K = 0;
+  long long lda = 0, ldw = 0;   // row pitches (elements)
+  const int8_t* aq = nullptr;
+  const float* a_scale = nullptr;
+  const int8_t* wq = nullptr;
+  float w_scale = 1.0f;
+  const __nv_bfloat16* ah = nullptr;
+  const __nv_bfloat16* wh = nullptr;
+  const float* af = nullptr;
+  const float* wf = nullptr;
+};
+void launch_shortlist_topk(int prec, const ShortlistArgs& a, const BeamDev& b, cudaStream_t st);
 void launch_softmax_topk(const float* logits, long long ldl, const float* part_m,
                          const float* part_s, const int* part_arg, long long part_ld,
                          const BeamDev& b, cudaStream_t st);

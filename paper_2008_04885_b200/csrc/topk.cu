@@ -222,6 +222,148 @@ __global__ void __launch_bounds__(kMT)
   }
 }
 
+
+// ---- vocabulary shortlist (decode.cpp:55-61 with rows; model.cpp:440-449) ----
+// One 128-thread CTA per live row r of sentence s with shortlist L_s (sorted
+// full-vocabulary ids, n = |L_s| <= kMaxShortlist): logits of the shortlist
+// rows only, then log_softmax over those n values (P6 over subset
+// positions, exactly as over a full row) and the top-kB by (score desc,
+// token asc) with token = L_s[j].
+//   int8 : acc = sum a_q * w_q (exact int32), x = float(acc) * (1/(sa*sw))
+//          -- the same value the full projection produces (qmatmul_nt rows).
+//   fp32 : 8 interleaved partial sums, ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7))
+//          (the oracle's dot8 stand-in for Eigen's dot, tensor.cpp:125-133).
+//   bf16 : bf16 operands, products summed in fp32 in k order.
+template <int PREC>
+__global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float lg[kMaxShortlist];
+  __shared__ float red_f[kMT / 32];
+  __shared__ int red_i[kMT / 32];
+  const int r = blockIdx.x;
+  if (r >= *b.n_rows) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = b.row_sent[r];
+  const int* ids = a.sl_ids + a.sl_off[s];
+  const int n = a.sl_off[s + 1] - a.sl_off[s];
+  const int K = a.K;
+  const float plp = b.row_lp[r];
+  float inv = 1.0f;
+  if constexpr (PREC == 0) inv = __frcp_rn(__fmul_rn(a.a_scale[r], a.w_scale));
+  for (int j = tid; j < n; j += kMT) {
+    const long long col = ids[j];
+    float x;
+    if constexpr (PREC == 0) {  // int8, K padded to 16 bytes
+      const int4* av = reinterpret_cast<const int4*>(a.aq + static_cast<long long>(r) * a.lda);
+      const int4* wv = reinterpret_cast<const int4*>(a.wq + col * a.ldw);
+      int acc = 0;
+      for (int k = 0; k < a.lda / 16; ++k) {
+        const int4 p = av[k], q = wv[k];
+        acc = __dp4a(p.x, q.x, acc);
+        acc = __dp4a(p.y, q.y, acc);
+        acc = __dp4a(p.z, q.z, acc);
+        acc = __dp4a(p.w, q.w, acc);
+      }
+      x = __fmul_rn(__int2float_rn(acc), inv);
+    } else if constexpr (PREC == 1) {
+      const __nv_bfloat16* ar = a.ah + static_cast<long long>(r) * a.lda;
+      const __nv_bfloat16* wr = a.wh + col * a.ldw;
+      float acc = 0.0f;
+      for (int k = 0; k < K; ++k)
+        acc = __fadd_rn(acc, __fmul_rn(__bfloat162float(ar[k]), __bfloat162float(wr[k])));
+      x = acc;
+    } else {
+      const float* ar = a.af + static_cast<long long>(r) * a.lda;
+      const float* wr = a.wf + col * a.ldw;
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int k = 0;
+      for (; k + 8 <= K; k += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = __fadd_rn(acc[u], __fmul_rn(ar[k + u], wr[k + u]));
+      for (; k < K; ++k) acc[k & 7] = __fadd_rn(acc[k & 7], __fmul_rn(ar[k], wr[k]));
+      x = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+    }
+    lg[j] = x;
+  }
+  __syncthreads();
+  // log-sum-exp in the P6 order over the n subset positions.
+  const int nsub = (n + 31) / 32;
+  float mloc = kNegInf;
+  float mv[kMaxShortlist / 32 / kMT + 1];
+  float sv[kMaxShortlist / 32 / kMT + 1];
+#pragma unroll
+  for (int i = 0; i < kMaxShortlist / 32 / kMT + 1; ++i) {
+    const int k = tid + kMT * i;
+    mv[i] = kNegInf;
+    sv[i] = 0.0f;
+    if (k < nsub) {
+      const int j0 = 32 * k, j1 = min(n, j0 + 32);
+      float best = kNegInf;
+      bool any = false;
+      for (int j = j0; j < j1; ++j)
+        if (lg[j] > best) {
+          best = lg[j];
+          any = true;
+        }
+      float sum = 0.0f;
+      if (any)
+        for (int j = j0; j < j1; ++j) sum = __fadd_rn(sum, det_expf_nonpos(__fsub_rn(lg[j], best)));
+      mv[i] = best;
+      sv[i] = sum;
+      mloc = fmaxf(mloc, best);
+    }
+  }
+  mloc = warp_allmax(mloc);
+  if (lane == 0) red_f[warp] = mloc;
+  __syncthreads();
+  const float M = fmaxf(fmaxf(red_f[0], red_f[1]), fmaxf(red_f[2], red_f[3]));
+  __syncthreads();
+  float part = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kMaxShortlist / 32 / kMT + 1; ++i)
+    if (tid + kMT * i < nsub) {
+      const float u =
+          mv[i] == kNegInf ? 0.0f : __fmul_rn(sv[i], det_expf_nonpos(__fsub_rn(mv[i], M)));
+      part = __fadd_rn(part, u);
+    }
+  part = warp_allsum(part);
+  if (lane == 0) red_f[warp] = part;
+  __syncthreads();
+  const float total = __fadd_rn(__fadd_rn(red_f[0], red_f[1]), __fadd_rn(red_f[2], red_f[3]));
+  __syncthreads();
+  const float lse = __fadd_rn(det_logf(total), M);
+  // Top-kB by (score desc, token asc), token = ids[j].
+  const int kB = min(b.B, n);
+  float last_s = kPosInf;
+  int last_t = -1;
+  for (int k = 0; k < kB; ++k) {
+    float bs = kNegInf;
+    int bt = INT_MAX;
+    for (int j = tid; j < n; j += kMT) {
+      const float sc = __fadd_rn(plp, __fsub_rn(lg[j], lse));
+      const int tk = ids[j];
+      if (sc == sc && better2(last_s, last_t, sc, tk) && (bt == INT_MAX || better2(sc, tk, bs, bt))) {
+        bs = sc;
+        bt = tk;
+      }
+    }
+    block_best(bs, bt, red_f, red_i);
+    if (tid == 0) {
+      b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
+      b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
+    }
+    if (bt == INT_MAX) break;
+    last_s = bs;
+    last_t = bt;
+  }
+  for (int k = kB + tid; k < b.B; k += kMT) {
+    b.cand_score[static_cast<long long>(r) * b.B + k] = kNegInf;
+    b.cand_tok[static_cast<long long>(r) * b.B + k] = INT_MAX;
+  }
+}
+
 }  // namespace
 
 long long topk_pitch(int V) {
@@ -230,6 +372,19 @@ long long topk_pitch(int V) {
 }
 
 long long softmax_part_pitch(int V) { return ((V + 31) / 32 + 3) / 4 * 4; }
+
+void launch_shortlist_topk(int prec, const ShortlistArgs& a, const BeamDev& b, cudaStream_t st) {
+  if (b.B > kMaxBeam) fail(kUsageError, "beam size above 16 is not supported");
+  if (prec == 0 && a.lda % 16 != 0) fail(kStateError, "shortlist: int8 operand pitch");
+  const dim3 grid(b.R_max), block(kMT);
+  if (prec == 0)
+    launch_k(shortlist_topk_kernel<0>, grid, block, 0, st, a, b);
+  else if (prec == 1)
+    launch_k(shortlist_topk_kernel<1>, grid, block, 0, st, a, b);
+  else
+    launch_k(shortlist_topk_kernel<2>, grid, block, 0, st, a, b);
+  MTG_CUDA(cudaGetLastError());
+}
 
 void launch_softmax_topk(const float* logits, long long ldl, const float* part_m,
                          const float* part_s, const int* part_arg, long long part_ld,

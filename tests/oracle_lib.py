@@ -39,6 +39,9 @@ def _load():
     lib.orc_set_param.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.c_longlong]
     lib.orc_get_qparam.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.c_longlong, _vp]
     lib.orc_pos_enc.argtypes = [_vp, _vp]
+    lib.orc_encode_factors.argtypes = [_vp, _c_int, _vp, _c_int, _vp, _c_int, _vp]
+    lib.orc_beam_search_factors.argtypes = [_vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int,
+                                            _c_float, _vp, _c_int, _vp, _vp, _vp, _vp]
     lib.orc_beam_search.argtypes = [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_float, _vp, _c_int,
                                     _vp, _c_int, _vp, _vp, _vp, _vp]
     lib.orc_translate_batch.argtypes = [_vp, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_float,
@@ -195,11 +198,32 @@ class OracleModel:
         check(lib.orc_teacher_forced(self.h, P(s), len(s), P(t), len(t), P(out)))
         return out
 
-    def encode(self, src, int8: bool = False) -> np.ndarray:
+    def encode(self, src, int8: bool = False, factors=None) -> np.ndarray:
         s = i32(src)
         out = np.zeros((len(s), self.config["d_model"]), np.float32)
-        check(lib.orc_encode(self.h, int(int8), P(s), len(s), P(out)))
+        if factors is not None:
+            f = i32(np.asarray(factors, np.int32).reshape(-1))
+            check(lib.orc_encode_factors(self.h, int(int8), P(s), len(s), P(f), len(factors), P(out)))
+        else:
+            check(lib.orc_encode(self.h, int(int8), P(s), len(s), P(out)))
         return out
+
+    def beam_search_factors(self, src, factors, beam: int, max_len: int, alpha: float = 1.0,
+                            int8: bool = False) -> dict:
+        """decode.hpp:35-38 with source-factor streams (each aligned with src)."""
+        s = i32(src)
+        f = i32(np.asarray(factors, np.int32).reshape(-1))
+        cap = max(max_len, 1) + 1
+        toks = np.zeros(cap, np.int32)
+        n = ctypes.c_int()
+        lp = ctypes.c_float()
+        nm = ctypes.c_float()
+        fl = ctypes.c_int()
+        check(lib.orc_beam_search_factors(self.h, int(int8), P(s), len(s), P(f), len(factors), beam,
+                                          max_len, alpha, P(toks), cap, ctypes.byref(n),
+                                          ctypes.byref(lp), ctypes.byref(nm), ctypes.byref(fl)))
+        return dict(tokens=toks[:n.value].tolist(), logprob=lp.value, norm=nm.value,
+                    finished=bool(fl.value & 1), truncated=bool(fl.value & 2))
 
 
 def quantize(x: np.ndarray):

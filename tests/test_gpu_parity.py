@@ -331,3 +331,74 @@ def test_step_fusion_modes_agree():
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
                                    capture_output=True, text=True).stdout)
     assert outs[0] == outs[1] == outs[2] and outs[0].strip()
+
+
+@pytest.mark.parametrize("combine,shared", [("concat", False), ("sum", False), ("average", True),
+                                            ("sum", True)])
+def test_source_factors_bit_exact(combine, shared):
+    """Source-factor embedding (model.cpp:539-581): concat / sum / average,
+    own or shared tables; encoder rows and int8 hypotheses bit-exact, f32
+    hypotheses identical."""
+    d = 16
+    fdim = 8 if combine == "concat" else d
+    factors = [dict(combine=combine, embed_dim=fdim, share=shared, vocab_size=9)]
+    if combine != "concat":
+        factors.append(dict(combine=combine, embed_dim=fdim, share=shared, vocab_size=7))
+    c = dict(cfg(2, 1, d, 32, 2, 20, 24, 32), factors=factors)
+    om = o.OracleModel.create(c, seed=17)
+    path = "/tmp/factors_%s_%d.bin" % (combine, int(shared))
+    om.save(path)
+    rng = np.random.default_rng(5)
+    srcs = o.synthetic_sources(5, 6, 20, seed=9)
+    facs = [[rng.integers(0, f["vocab_size"], len(s)).tolist() for f in factors] for s in srcs]
+    for prec, int8 in ((mt.INT8, True), (mt.F32, False)):
+        gm = mt.Model.load(path, precision=prec)
+        enc = gm.encode(srcs, factors=facs)
+        ref = np.concatenate([om.encode(s, int8, factors=f) for s, f in zip(srcs, facs)])
+        if int8:
+            assert np.array_equal(enc.view(np.uint32), ref.view(np.uint32))
+        else:
+            assert rel(enc, ref) < 1e-4
+        hyps = gm.translate(srcs, mt.BeamConfig(4, 0, 1.0), factors=facs)
+        for s, f, h in zip(srcs, facs, hyps):
+            r = om.beam_search_factors(s, f, 4, derive(s, 32), 1.0, int8)
+            assert h.tokens == r["tokens"]
+            if int8:
+                assert f32hex(h.logprob) == f32hex(r["logprob"])
+    # contract errors (model.cpp:541-546, tensor.cpp:456-458)
+    gm = mt.Model.load(path, precision=mt.INT8)
+    assert gm.translate(srcs[:1], mt.BeamConfig(2, 0, 1.0))[0].status == 1  # ShapeError: no streams
+    bad = [[list(x) for x in facs[0]]]
+    bad[0][0][0] = 999
+    assert gm.translate(srcs[:1], mt.BeamConfig(2, 0, 1.0), factors=bad)[0].status == 3  # IndexError
+
+
+def test_vocabulary_shortlist_bit_exact():
+    """Shortlist decoding (decode.cpp:344-349, model.cpp:440-449): logits,
+    log-softmax and candidates over the sentence's shortlist only, candidate
+    token = full-vocabulary id; mixed batches (with and without a shortlist)
+    and per-sentence errors."""
+    c = cfg(2, 2, 32, 64, 4, 300, 600, 48)
+    om = o.OracleModel.create(c, seed=23)
+    path = "/tmp/shortlist.bin"
+    om.save(path)
+    rng = np.random.default_rng(3)
+    srcs = o.synthetic_sources(6, 7, 300, seed=12)
+    sls = [sorted(set([0, 1, 2, 3]) | set(rng.choice(600, 60, replace=False).tolist())) for _ in srcs]
+    sls[4] = []  # this sentence decodes over the full vocabulary
+    for prec, int8 in ((mt.INT8, True), (mt.F32, False)):
+        gm = mt.Model.load(path, precision=prec)
+        hyps = gm.translate(srcs, mt.BeamConfig(5, 0, 1.0), shortlists=sls)
+        for s, sl, h in zip(srcs, sls, hyps):
+            r = om.beam_search(s, 5, derive(s, 48), 1.0, int8, shortlist=sl if sl else None)
+            assert h.status == 0
+            assert h.tokens == r["tokens"]
+            assert not sl or set(h.tokens) <= set(sl)
+            if int8:
+                assert f32hex(h.logprob) == f32hex(r["logprob"])
+        h1 = mt.beam_search(gm, srcs[0], (), mt.BeamConfig(5, 0, 1.0), shortlist=sls[0])
+        assert h1.tokens == hyps[0].tokens
+    gm = mt.Model.load(path, precision=mt.INT8)
+    bad = [list(sls[0]), sls[1][:-1] + [600], list(reversed(sls[2]))]
+    st = [h.status for h in gm.translate(srcs[:3], mt.BeamConfig(3, 0, 1.0), shortlists=bad)]
+    assert st == [0, 3, 6]  # ok, IndexError (bad row), UsageError (unsorted)
