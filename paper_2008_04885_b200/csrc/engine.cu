@@ -21,6 +21,17 @@ namespace {
 int gemm_prec_of(int prec) {
   return prec == kINT8 ? kPrecI8 : prec == kBF16 ? kPrecBF16 : kPrecTF32x3;
 }
+// Activation operands: fp32 activations stay plain fp32 (the GEMM splits
+// them into tf32 hi + lo in shared memory, gemm_tc.cuh kPrecTF32x3A).
+// MTG_F32_SPLIT_A=1 selects that in-kernel split (A/B: measured slower with
+// the two-stage fp32 pipelines); by default producers write hi + lo.
+int act_prec_of(int prec) {
+  static const bool split_a = [] {
+    const char* e = std::getenv("MTG_F32_SPLIT_A");
+    return e && e[0] == '1';
+  }();
+  return prec == kF32 && split_a ? kPrecTF32x3A : gemm_prec_of(prec);
+}
 
 
 // Converts fp32 K-major rows (host, [n x k]) into the operand format.
@@ -130,6 +141,8 @@ void ActOperand::allocate(int rows_, int k_, int prec_) {
     row_scale.resize(rows);
   } else if (prec == kPrecBF16) {
     h.resize(n);
+  } else if (prec == kPrecTF32x3A) {
+    hi.resize(n);  // plain fp32
   } else {
     hi.resize(n);
     lo.resize(n);
@@ -279,9 +292,10 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   const int N = cap_sent_, M = cap_enc_, B = cap_beam_;
   r_max_ = N * B;
   act_rows_ = std::max(M, r_max_);
-  const int gp = gemm_prec_of(prec_);
+  const int gp = act_prec_of(prec_);
   act_d_.allocate(act_rows_, d_, gp);
   act_ff_.allocate(act_rows_, dff_, gp);
+  if (prec_ == kF32) act_logits_.allocate(act_rows_, d_, kPrecTF32x3);  // hi + lo for the projection
   const size_t d = d_, dff = dff_;
   enc_x_.resize(M * d);
   enc_a_.resize(M * d);
@@ -400,16 +414,17 @@ void Engine::prep(const float* x, long long ldx, int k, int max_rows, const int*
                            out.row_scale.get(), nonfinite_.get(), stream_);
   } else if (prec_ == kBF16) {
     launch_cast_bf16(x, ldx, k, max_rows, d_rows, out.h.get(), out.k_pad, stream_);
-  } else {
-    launch_split_tf32(x, ldx, k, max_rows, d_rows, out.hi.get(), out.lo.get(), out.k_pad,
-                      stream_);
+  } else {  // kPrecTF32x3A: plain copy (lo == null); kPrecTF32x3: hi + lo
+    launch_split_tf32(x, ldx, k, max_rows, d_rows, out.hi.get(),
+                      out.prec == kPrecTF32x3 ? out.lo.get() : nullptr, out.k_pad, stream_);
   }
   count("operand prep");
 }
 
 void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
                   long long ldc, const float* bias, const float* residual, int relu,
-                  long long c_step_stride, const int* d_step, unsigned* seg_absmax) {
+                  long long c_step_stride, const int* d_step, unsigned* seg_absmax,
+                  float* c_lo) {
   auto& cache = plan_cache(this);
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
@@ -430,6 +445,7 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   ep.M = m;
   ep.d_M = d_m;
   ep.N = w.n;
+  ep.C_lo = c_lo;
   if (seg_absmax) {
     if (residual) fail(kStateError, "gemm: sentence-max epilogue takes no residual");
     ep.seg_absmax = seg_absmax;
@@ -527,7 +543,8 @@ ShortlistArgs Engine::shortlist_args() const {
 
 void Engine::gemm_logits(int m, const int* d_m) {
   auto& cache = plan_cache(this);
-  PlanKey key{act_d_.op().ptr, logits_w_.op().ptr, m};
+  ActOperand& la = logits_act();
+  PlanKey key{la.op().ptr, logits_w_.op().ptr, m};
   auto it = cache.find(key);
   // Persistent double-buffered kernel for TF32x3 (MMA-bound); the int8 / bf16
   // projection is epilogue-bound and measured faster as one tile per CTA at
@@ -539,14 +556,14 @@ void Engine::gemm_logits(int m, const int* d_m) {
   const bool persistent = persistent_env >= 0 ? persistent_env != 0 : prec_ == kF32;
   if (it == cache.end())
     it = cache
-             .emplace(key, persistent ? plan_logits(act_d_.op(), logits_w_.op(), m, logits_w_.n)
-                                      : plan_gemm(act_d_.op(), logits_w_.op(), m, logits_w_.n,
-                                                  0, 128))
+             .emplace(key, persistent ? plan_logits(la.op(), logits_w_.op(), m, logits_w_.n)
+                                      : plan_gemm(la.op(), logits_w_.op(), m, logits_w_.n, 0,
+                                                  128))
              .first;
   GemmEpilogue ep{};
   ep.C = logits_.get();
   ep.ldc = Vp_;
-  ep.a_scale = act_d_.row_scale.get();
+  ep.a_scale = la.row_scale.get();
   ep.w_seg_scale = logits_w_.seg_scale.get();
   ep.seg_width = logits_w_.seg_width;
   ep.M = m;
@@ -740,11 +757,15 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     EncLayer& L = enc_[l];
     ln_enc(enc_x_.get(), m, L.n1, enc_a_.get(), act_d_);
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
+    const bool plain = prec_is_tf32x3(act_d_.prec);  // fp32: contexts are the operand
     launch_enc_attention(enc_qkv_.get(), 3 * d, src_off_.get(), n_sent, std::max(max_src, 1), d_,
-                         heads_, scale, enc_ctx_.get(), d, fused ? sent_absmax_.get() : nullptr,
-                         nonfinite_.get(), stream_);
+                         heads_, scale, plain ? act_d_.hi.get() : enc_ctx_.get(),
+                         plain ? act_d_.k_pad : d,
+                         act_d_.prec == kPrecTF32x3 ? act_d_.lo.get() : nullptr,
+                         fused ? sent_absmax_.get() : nullptr, nonfinite_.get(), stream_);
     count("enc attention");
-    if (fused) {
+    if (plain) {
+    } else if (fused) {
       launch_quantize_sent(enc_ctx_.get(), d, m, d_, src_rowseg_.get(), sent_absmax_.get(), od,
                            stream_);
       count("enc quantize (sentence max)");
@@ -753,9 +774,15 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     }
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
     ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
-    gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1, 0, nullptr,
-         fused ? sent_absmax_.get() : nullptr);
-    if (fused) {
+    if (plain) {
+      gemm(act_d_, L.w1, m, nullptr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
+           nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
+    } else {
+      gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1, 0, nullptr,
+           fused ? sent_absmax_.get() : nullptr);
+    }
+    if (plain) {
+    } else if (fused) {
       launch_quantize_sent(ffh_.get(), dff_, m, dff_, src_rowseg_.get(), sent_absmax_.get(), off_,
                            stream_);
       count("enc quantize (sentence max)");
@@ -864,11 +891,21 @@ void Engine::decoder_body(bool reorder) {
     count("cross attention");
     gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
     ln_dec(L.n3);
-    gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
-    prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
+    if (prec_is_tf32x3(act_ff_.prec)) {  // FFN-up writes the FFN-down operand itself
+      gemm(act_d_, L.w1, R, dr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
+           nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
+    } else {
+      gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
+      prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
+    }
     gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
   }
-  if (c.num_decoder_layers > 0) ln_dec(dec_final_, final_y);
+  if (c.num_decoder_layers > 0) {
+    const OperandOut ol = opout(logits_act());
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, dec_final_.g.get(), dec_final_.b.get(), final_y,
+                     d, nullptr, &ol, stream_);
+    count("layernorm");
+  }
   if (!use_shortlist_) gemm_logits(R, dr);  // shortlists project inside their top-k kernel
 }
 

@@ -112,7 +112,7 @@ class Engine {
   void gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
             long long ldc, const float* bias, const float* residual, int relu,
             long long c_step_stride = 0, const int* d_step = nullptr,
-            unsigned* seg_absmax = nullptr);
+            unsigned* seg_absmax = nullptr, float* c_lo = nullptr);
   // Output projection into logits_ plus the per-slice softmax partials.
   void gemm_logits(int m, const int* d_m);
   int stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status);
@@ -173,6 +173,8 @@ class Engine {
   int cap_sent_ = 0, cap_enc_ = 0, cap_beam_ = 0, r_max_ = 0, act_rows_ = 0;
   int d_ = 0, dff_ = 0, V_ = 0, Vp_ = 0, T_ = 0, heads_ = 0;
   ActOperand act_d_, act_ff_;
+  ActOperand act_logits_;  // fp32: hi + lo operand of the output projection
+  ActOperand& logits_act() { return prec_ == kF32 ? act_logits_ : act_d_; }
   DeviceBuffer<float> enc_x_, enc_a_, enc_qkv_, enc_ctx_, ffh_;
   std::vector<DeviceBuffer<float>> ckv_;
   DeviceBuffer<float> dec_y_, dec_a_, dec_ctx_, dec_cq_, logits_;

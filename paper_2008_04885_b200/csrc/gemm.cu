@@ -96,6 +96,17 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
     }
     fail(kStateError, "gemm: softmax partials need a 128/256-column tile");
   }
+  if (ep.C_lo) {
+    if constexpr (prec_is_tf32x3(PREC)) {
+      switch (p.bn) {
+        case 32: return launch_one<PREC, 32, kEpiTf32Out>(p, ep, stream);
+        case 64: return launch_one<PREC, 64, kEpiTf32Out>(p, ep, stream);
+        case 128: return launch_one<PREC, 128, kEpiTf32Out>(p, ep, stream);
+        case 256: return launch_one<PREC, 256, kEpiTf32Out>(p, ep, stream);
+      }
+    }
+    fail(kStateError, "gemm: TF32 operand output needs a TF32x3 GEMM");
+  }
   if (ep.seg_absmax) {
     if (ep.residual) fail(kStateError, "gemm: segment-max epilogue takes no residual");
     switch (p.bn) {
@@ -118,7 +129,8 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
 
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn,
                    int min_bn, bool allow_split) {
-  if (a.prec != b.prec || a.k_pad != b.k_pad)
+  const bool split_a = a.prec == kPrecTF32x3A && b.prec == kPrecTF32x3;  // plain fp32 A
+  if ((a.prec != b.prec && !split_a) || a.k_pad != b.k_pad)
     fail(kShapeError, "gemm: operand precision / K mismatch");
   if (a.k_pad % (128 / prec_elem_bytes(a.prec)) != 0)
     fail(kShapeError, "gemm: K not padded to a 128-byte slab");
@@ -165,13 +177,15 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   p.smem = p.nst * stage + kGemmSmemExtra;
   p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, bn);
-  if (a.prec == kPrecTF32x3) {
-    if (!a.ptr_lo || !b.ptr_lo) fail(kStateError, "gemm: TF32x3 needs lo operands");
-    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 128);
+  p.a2 = p.a;
+  p.b2 = p.b;
+  if (prec_is_tf32x3(b.prec)) {
+    if (!b.ptr_lo) fail(kStateError, "gemm: TF32x3 needs the weight lo part");
     p.b2 = make_map(b.ptr_lo, b.prec, b.rows, b.k_pad, bn);
-  } else {
-    p.a2 = p.a;
-    p.b2 = p.b;
+  }
+  if (a.prec == kPrecTF32x3) {
+    if (!a.ptr_lo) fail(kStateError, "gemm: TF32x3 needs the activation lo part");
+    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 128);
   }
   return p;
 }
@@ -235,6 +249,7 @@ void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
     case kPrecI8: return launch_prec<kPrecI8>(p, ep, stream);
     case kPrecBF16: return launch_prec<kPrecBF16>(p, ep, stream);
     case kPrecTF32x3: return launch_prec<kPrecTF32x3>(p, ep, stream);
+    case kPrecTF32x3A: return launch_prec<kPrecTF32x3A>(p, ep, stream);
   }
   fail(kStateError, "gemm: unknown precision");
 }

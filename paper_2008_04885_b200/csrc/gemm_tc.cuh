@@ -59,15 +59,37 @@ struct GemmEpilogue {
   unsigned* seg_absmax;
   const int* row_seg;
   int* nonfinite;
+  // Optional: write the output as a TF32x3 operand, C = tf32(y), C_lo = y - C
+  // (the next GEMM's A), instead of plain y.
+  float* C_lo;
 };
+
+// Stores y at C[off] (or its tf32 hi / lo split for the kEpiTf32Out epilogue).
+template <bool kTf32Out>
+__device__ __forceinline__ void gemm_store(float* C, float* C_lo, long long off, float y) {
+  if constexpr (kTf32Out) {
+    uint32_t hb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(y));
+    C[off] = __uint_as_float(hb);
+    C_lo[off] = __fsub_rn(y, __uint_as_float(hb));
+  } else {
+    C[off] = y;
+  }
+}
 
 // EPI = 0: linear-layer epilogue. EPI = 1: output projection; also emits the
 // log-softmax / top-k partials (no bias, relu or residual).
 constexpr int kEpiLinear = 0;
 constexpr int kEpiSoftmaxParts = 1;
 constexpr int kEpiSegMax = 2;  // linear + per-segment max |y| (bias/ReLU in phase 1)
+constexpr int kEpiTf32Out = 3;  // linear, output written as a TF32x3 operand (hi + lo)
 
-enum GemmPrec : int { kPrecI8 = 0, kPrecBF16 = 1, kPrecTF32x3 = 2 };
+// kPrecTF32x3A: TF32x3 whose A operand arrives as plain fp32 and is split
+// into hi + lo inside the kernel (half the activation bytes); B as kPrecTF32x3.
+enum GemmPrec : int { kPrecI8 = 0, kPrecBF16 = 1, kPrecTF32x3 = 2, kPrecTF32x3A = 3 };
+__host__ __device__ constexpr bool prec_is_tf32x3(int prec) {
+  return prec == kPrecTF32x3 || prec == kPrecTF32x3A;
+}
 
 constexpr int kMaxSegments = 4;
 constexpr int kMaxStages = 8;
@@ -81,7 +103,7 @@ __host__ __device__ constexpr int prec_mma_kind(int prec) {
   return prec == kPrecI8 ? kKindI8 : prec == kPrecBF16 ? kKindF16 : kKindTF32;
 }
 __host__ __device__ constexpr int gemm_stage_bytes(int prec, int bn) {
-  return (128 * 128 + bn * 128) * (prec == kPrecTF32x3 ? 2 : 1);
+  return (128 * 128 + bn * 128) * (prec_is_tf32x3(prec) ? 2 : 1);
 }
 __host__ __device__ constexpr int gemm_tmem_cols(int bn) {
   return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
@@ -96,7 +118,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
                    const __grid_constant__ CUtensorMap mapA2,
                    const __grid_constant__ CUtensorMap mapB2, int num_kb, int nst,
                    GemmEpilogue ep) {
-  constexpr bool kSplit = (PREC == kPrecTF32x3);
+  constexpr bool kSplit = prec_is_tf32x3(PREC);
+  constexpr bool kSplitA = (PREC == kPrecTF32x3A);  // A split by the epilogue warps
   constexpr int kKind = prec_mma_kind(PREC);
   constexpr int kElem = prec_elem_bytes(PREC);
   constexpr int kKbElems = 128 / kElem;      // K elements per 128-byte slab
@@ -120,7 +143,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * kStageBytes);
   uint64_t* empty_bar = full_bar + kMaxStages;
   uint64_t* accum_bar = empty_bar + kMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+  uint64_t* conv_bar = accum_bar + 1;  // [kMaxStages] A split done (kSplitA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv_bar + kMaxStages);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -139,6 +163,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+      mbar_init(&conv_bar[s], kEpiWarps);
     }
     mbar_init(accum_bar, 1);
     fence_barrier_init();
@@ -152,8 +177,9 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   // their first stages before the programmatic-dependency wait, so the weight
   // fetch overlaps the predecessor's tail. Everything that reads predecessor
   // outputs (A operand, row count, scales, residual) comes after pdl_wait.
-  constexpr int kABytes = kATile * (kSplit ? 2 : 1);
+  constexpr int kABytes = kATile * (kSplit && !kSplitA ? 2 : 1);  // A bytes loaded by TMA
   constexpr int kBBytes = kBTile * (kSplit ? 2 : 1);
+  constexpr int kLoadBytes = kABytes + kBBytes;
   const int npre = min(nst, kb_count);
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < npre; ++kb) {
@@ -190,15 +216,16 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         if (kb < npre) {  // B already in flight
           mbar_arrive_expect_tx(&full_bar[s], kABytes);
           tma_load_2d(st, &mapA, &full_bar[s], kx, m0);
-          if constexpr (kSplit) tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kx, m0);
+          if constexpr (kSplit && !kSplitA)
+            tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kx, m0);
           continue;
         }
         mbar_wait(&empty_bar[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+        mbar_arrive_expect_tx(&full_bar[s], kLoadBytes);
         tma_load_2d(st, &mapA, &full_bar[s], kx, m0);
         tma_load_2d(st + kATile, &mapB, &full_bar[s], kx, n0);
         if constexpr (kSplit) {
-          tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kx, m0);
+          if constexpr (!kSplitA) tma_load_2d(st + kATile + kBTile, &mapA2, &full_bar[s], kx, m0);
           tma_load_2d(st + 2 * kATile + kBTile, &mapB2, &full_bar[s], kx, n0);
         }
       }
@@ -215,7 +242,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       for (int kb = 0; kb < kb_count; ++kb) {
         const int s = kb % nst;
         const uint32_t ph = (kb / nst) & 1;
-        mbar_wait(&full_bar[s], ph);
+        mbar_wait(kSplitA ? &conv_bar[s] : &full_bar[s], ph);
         tc_fence_after();
         const uint32_t a_base = smem_u32(smem + s * kStageBytes);
         const uint32_t b_base = a_base + kATile;
@@ -244,6 +271,33 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       cluster_sync_all();
     }
   } else {
+    if constexpr (kSplitA) {
+      // ---- A split: the epilogue warps turn each landed fp32 A slab into
+      // tf32 hi (in place) + lo (the A-lo slot) while the MMAs run ----
+      const int t = threadIdx.x - 64;  // 0..255
+      for (int kb = 0; kb < kb_count; ++kb) {
+        const int s = kb % nst;
+        mbar_wait(&full_bar[s], (kb / nst) & 1);
+        float* a = reinterpret_cast<float*>(smem + s * kStageBytes);
+        float* alo = reinterpret_cast<float*>(smem + s * kStageBytes + kATile + kBTile);
+#pragma unroll
+        for (int i = 4 * t; i < kATile / 4; i += 4 * 256) {
+          float4 v = *reinterpret_cast<const float4*>(a + i);
+          float4 h;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t*>(&h.x)) : "f"(v.x));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t*>(&h.y)) : "f"(v.y));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t*>(&h.z)) : "f"(v.z));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t*>(&h.w)) : "f"(v.w));
+          *reinterpret_cast<float4*>(a + i) = h;
+          *reinterpret_cast<float4*>(alo + i) =
+              make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z),
+                          __fsub_rn(v.w, h.w));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv_bar[s]);
+      }
+    }
     // ---- epilogue: TMEM -> registers -> smem transpose -> coalesced global ----
     // Phase 1 (thread = row): convert a 32 x kChunk accumulator sub-tile
     // (int8: x 1/(sa*sw), reciprocal hoisted per weight segment) into padded
@@ -433,6 +487,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       const int col = n0 + c + (lane % kChunk);
       const bool col_ok = col < N && lane < kChunk;
       float* cp = Cbase + col;
+      float* cp_lo = EPI == kEpiTf32Out ? ep.C_lo + (cp - ep.C) : nullptr;
       if constexpr (kPrefetch) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -440,7 +495,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
           if (has_bias && !seg_mode) x = __fadd_rn(x, bias_pre);
           if (relu && !seg_mode) x = x > 0.0f ? x : 0.0f;
           if (has_res) x = __fadd_rn(res_pre[i], x);
-          if (col_ok && i < nrows) cp[i * ldc] = x;
+          if (col_ok && i < nrows) gemm_store<EPI == kEpiTf32Out>(cp, cp_lo, i * ldc, x);
         }
         __syncwarp();
         continue;
@@ -449,7 +504,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         if (col_ok) {
 #pragma unroll 8
           for (int i = 0; i < 32; ++i)
-            if (i < nrows) cp[i * ldc] = stage[i * 33 + lane];
+            if (i < nrows) gemm_store<EPI == kEpiTf32Out>(cp, cp_lo, i * ldc, stage[i * 33 + lane]);
         }
         __syncwarp();
         continue;
@@ -472,7 +527,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
           if (has_bias) x = __fadd_rn(x, bias);
           if (relu) x = x > 0.0f ? x : 0.0f;
           if (has_res) x = __fadd_rn(res[i], x);
-          if (col_ok && i0 + i < nrows) cp[(i0 + i) * ldc] = x;
+          if (col_ok && i0 + i < nrows) gemm_store<EPI == kEpiTf32Out>(cp, cp_lo, (i0 + i) * ldc, x);
         }
       }
       __syncwarp();

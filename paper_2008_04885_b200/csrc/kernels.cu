@@ -39,6 +39,9 @@ __device__ __forceinline__ void write_operand(const OperandOut& o, long long r, 
   } else if (o.prec == 1) {
     __nv_bfloat16* h = o.h + r * o.k_pad;
     for (int c = tid; c < o.k_pad; c += stride) h[c] = __float2bfloat16_rn(c < n ? x[c] : 0.0f);
+  } else if (o.prec == 3) {  // plain fp32 (split into tf32 hi + lo by the GEMM)
+    float* h = o.hi + r * o.k_pad;
+    for (int c = tid; c < o.k_pad; c += stride) h[c] = c < n ? x[c] : 0.0f;
   } else {
     float* hi = o.hi + r * o.k_pad;
     float* lo = o.lo + r * o.k_pad;
@@ -174,6 +177,14 @@ __device__ __forceinline__ void ln_row_regs(float (&xv)[KPL], const float (&gv)[
       if (c < op.k_pad) h[c] = __float2bfloat16_rn(c < n ? xv[i] : 0.0f);
     }
     for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) h[c] = __float2bfloat16_rn(0.0f);
+  } else if (op.prec == 3) {  // plain fp32
+    float* h = op.hi + r * op.k_pad;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < op.k_pad) h[c] = c < n ? xv[i] : 0.0f;
+    }
+    for (int c = 32 * KPL + lane; c < op.k_pad; c += 32) h[c] = 0.0f;
   } else {
     float* hi = op.hi + r * op.k_pad;
     float* lo = op.lo + r * op.k_pad;
@@ -589,6 +600,7 @@ template <int DH>
 __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ldq,
                                      const int* __restrict__ off, int d, int dh_rt, int max_len,
                                      float scale, float* __restrict__ ctx, long long ldc,
+                                     float* __restrict__ ctx_lo,
                                      unsigned* __restrict__ sent_absmax, int* nonfinite) {
   pdl_wait();
   pdl_trigger();
@@ -633,6 +645,16 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
       for (int c = lane; c < dh; c += 32) {  // lane wrote these itself
         mx = fmaxf(mx, fabsf(out[c]));
         bad |= !isfinite(out[c]);
+      }
+    }
+    if (ctx_lo) {  // fp32 path: the context row is the next GEMM's hi + lo operand
+      float* lo = ctx_lo + (out - ctx);
+      for (int c = lane; c < dh; c += 32) {
+        const float v = out[c];
+        uint32_t hb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+        out[c] = __uint_as_float(hb);
+        lo[c] = __fsub_rn(v, __uint_as_float(hb));
       }
     }
   }
@@ -994,7 +1016,7 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
                           int max_len, int d, int heads, float scale, float* ctx, long long ldc,
-                          unsigned* sent_absmax, int* nonfinite, cudaStream_t st) {
+                          float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st) {
   if (n_sent <= 0) return;
   const int dh = d / heads;
   const int nw = 8;
@@ -1012,7 +1034,7 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
     cfg = smem;
   }
   launch_k(k, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale, ctx,
-           ldc, sent_absmax, nonfinite);
+           ldc, ctx_lo, sent_absmax, nonfinite);
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -154,6 +154,10 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, long long ld_x, i
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k_pad;
        c += gridDim.x * blockDim.x) {
     const float v = c < k ? x[r * ld_x + c] : 0.0f;
+    if (!lo) {  // plain fp32 operand (the GEMM splits it)
+      hi[static_cast<long long>(r) * k_pad + c] = v;
+      continue;
+    }
     uint32_t h;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
     const float hf = __uint_as_float(h);
