@@ -12,7 +12,7 @@
 //                     lse = log(S) + M. (log_softmax_row; the GPU computes the
 //                     slices in the output-projection GEMM epilogue)
 //   P3 dot          : acc = 0; acc = acc + a[c]*b[c] for c ascending (no FMA).
-//   attention ctx   : ctx[c] = P1 sum over keys j of p_j * v_j[c].
+//   attention ctx   : ctx[c] = sum over keys j ascending of p_j * v_j[c].
 //   P4 exp/log/pow  : detmath.h.
 //   P5 f32 GEMM     : per output element, k-ascending mul+add (gemm_rows order,
 //                     tensor.cpp:113-123); the GPU uses 3xTF32 tensor cores,
@@ -703,13 +703,12 @@ void attend_row(const float* q, const float* K, Index ldk, const float* V, Index
   for (Index j = 0; j < n; ++j) s[j] = orc_expf(s[j] - mx);
   const float sum = warp_sum(s.data(), n);
   for (Index j = 0; j < n; ++j) s[j] = s[j] / sum;
-  // ctx[c] = P1 sum over keys of p_j * v_j[c] (the GPU's lanes own keys and
-  // reduce-scatter the per-column partials; same tree as P1).
-  static thread_local std::vector<float> prod;
-  prod.resize(static_cast<size_t>(n));
+  // ctx[c] = sum over keys in ascending order of p_j * v_j[c] (the GPU's
+  // lanes own columns and walk the keys; model.cpp:649-650 P.V).
   for (Index c = 0; c < dh; ++c) {
-    for (Index j = 0; j < n; ++j) prod[j] = s[j] * V[j * ldv + c];
-    ctx[c] = warp_sum(prod.data(), n);
+    float acc = 0.0f;
+    for (Index j = 0; j < n; ++j) acc = acc + s[j] * V[j * ldv + c];
+    ctx[c] = acc;
   }
 }
 

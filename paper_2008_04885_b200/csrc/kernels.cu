@@ -477,24 +477,6 @@ __global__ void quantize_sent_kernel(const float* __restrict__ x, long long ldx,
 
 // ---- attention ---------------------------------------------------------------------------
 
-// Sums 32 per-lane partial vectors: lane l returns sum over lanes of a[l].
-// Pairs lanes differing in bit 4, then 3, ..., 0 -- the same tree as the
-// xor-butterfly P1 sum, so each column is bit-identical to warp_allsum.
-__device__ __forceinline__ float reduce_scatter32(float (&a)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool upper = (lane & w) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = upper ? a[i] : a[i + w];
-      const float keep = upper ? a[i + w] : a[i];
-      a[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, w));
-    }
-  }
-  return a[0];
-}
-
 // Shared-memory float4 load the compiler cannot hoist out of the key loop
 // (keeping q in registers would spill at the 80-register occupancy target).
 __device__ __forceinline__ float4 lds_f4(const float* p) {
@@ -506,8 +488,8 @@ __device__ __forceinline__ float4 lds_f4(const float* p) {
 }
 
 // One query against n keys, one warp. q: dh floats in smem (16-byte aligned);
-// s: n floats of per-warp smem scratch. P3 dots, P1 sums (softmax denominator
-// and context). DH > 0 fixes the head dim at compile time (float4 paths, all
+// s: n floats of per-warp smem scratch. P3 dots, P1 softmax denominator,
+// context summed over keys in ascending order per column. DH > 0 fixes the head dim at compile time (float4 paths, all
 // of a key row's loads issued before its dot product); DH == 0 is generic.
 // Key/value rows must be 16-byte aligned when DH % 4 == 0.
 template <int DH, class KP, class VP>
@@ -553,40 +535,20 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh_rt, fl
   const float sum = warp_allsum(part);
   for (int j = lane; j < n; j += 32) s[j] = __fdiv_rn(s[j], sum);
   __syncwarp();
-  // Context: lanes own keys j = lane + 32u and accumulate p_j * v_j[c] for a
-  // 32-column chunk, then a reduce-scatter butterfly leaves column c0+lane in
-  // lane `lane` (per column the same tree as the P1 warp sum).
+  // Context: lane owns columns lane, lane + 32, ... and walks the keys in
+  // ascending order (ctx[c] = sum_j p_j * v_j[c], oracle attend_row).
 #pragma unroll 1
-  for (int c0 = 0; c0 < (DH > 0 ? DH : 4096); c0 += 32) {
-    if (DH == 0 && c0 >= dh) break;
-    float acc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
-    for (int j = lane; j < n; j += 32) {
+  for (int c0 = 0; c0 < dh; c0 += 64) {
+    const int ca = c0 + lane, cb = c0 + 32 + lane;
+    float acc_a = 0.0f, acc_b = 0.0f;
+    for (int j = 0; j < n; ++j) {
       const float p = s[j];
-      const float* v = vp(j) + c0;
-      if constexpr (kVec && DH % 32 == 0) {
-#pragma unroll
-        for (int g = 0; g < 32; g += 16) {
-          float4 f[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) f[i] = *reinterpret_cast<const float4*>(v + g + 4 * i);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[g + 4 * i] = __fadd_rn(acc[g + 4 * i], __fmul_rn(p, f[i].x));
-            acc[g + 4 * i + 1] = __fadd_rn(acc[g + 4 * i + 1], __fmul_rn(p, f[i].y));
-            acc[g + 4 * i + 2] = __fadd_rn(acc[g + 4 * i + 2], __fmul_rn(p, f[i].z));
-            acc[g + 4 * i + 3] = __fadd_rn(acc[g + 4 * i + 3], __fmul_rn(p, f[i].w));
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          acc[i] = __fadd_rn(acc[i], __fmul_rn(p, c0 + i < dh ? v[i] : 0.0f));
-      }
+      const float* v = vp(j);
+      if (ca < dh) acc_a = __fadd_rn(acc_a, __fmul_rn(p, v[ca]));
+      if (cb < dh) acc_b = __fadd_rn(acc_b, __fmul_rn(p, v[cb]));
     }
-    const float col = reduce_scatter32(acc);
-    if (c0 + lane < dh) out[c0 + lane] = col;
+    if (ca < dh) out[ca] = acc_a;
+    if (cb < dh) out[cb] = acc_b;
   }
   __syncwarp();
 }
@@ -698,7 +660,7 @@ __host__ __device__ constexpr int round4(int x) { return (x + 3) & ~3; }
 // Key and value rows are copied global -> shared with cp.async, a whole row
 // per half-warp (coalesced), into a per-warp stage with an XOR swizzle of the
 // 16-byte columns, so the lane-per-key reads that follow are conflict-free.
-// Same arithmetic (P3 dots, P1 softmax, P1 context) as attend_warp<64>.
+// Same arithmetic (P3 dots, P1 softmax, key-ordered context) as attend_warp<64>.
 constexpr int kStageFloats = 32 * 64;  // one 32-key chunk of 64-float rows
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
@@ -723,20 +685,6 @@ __device__ __forceinline__ void stage_rows64(float* stage, int c0, int n, KP kp,
   for (int i = 0; i < 16; ++i) {
     const int jr = 2 * i + half, j = c0 + jr;
     if (j < n) cp_async16(stage + jr * 64 + ((c ^ (jr & 15)) << 2), kp(j) + 4 * c);
-  }
-  cp_async_commit();
-}
-
-// Columns col0 .. col0+31 of rows c0 .. c0+31 as [32][32]; float4 column c of
-// row jr at c ^ (jr & 7).
-template <class VP>
-__device__ __forceinline__ void stage_half32(float* stage, int c0, int n, int col0, VP vp,
-                                             int lane) {
-  const int c = lane & 7, q4 = lane >> 3;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int jr = 4 * i + q4, j = c0 + jr;
-    if (j < n) cp_async16(stage + jr * 32 + ((c ^ (jr & 7)) << 2), vp(j) + col0 + 4 * c);
   }
   cp_async_commit();
 }
@@ -768,7 +716,7 @@ __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, floa
     }
     __syncwarp();
   }
-  stage_half32(stage, 0, n, 0, vp, lane);  // first value chunk overlaps the softmax
+  stage_rows64(stage, 0, n, vp, lane);  // first value chunk overlaps the softmax
   mx = warp_allmax(mx);
   float part = 0.0f;
   for (int j = lane; j < n; j += 32) {
@@ -779,31 +727,24 @@ __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, floa
   const float sum = warp_allsum(part);
   for (int j = lane; j < n; j += 32) s[j] = __fdiv_rn(s[j], sum);
   __syncwarp();
-#pragma unroll 1
-  for (int cc = 0; cc < 2; ++cc) {
-    float acc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      if (cc != 0 || c0 != 0) stage_half32(stage, c0, n, 32 * cc, vp, lane);
-      cp_async_wait_warp();
-      const int j = c0 + lane;
-      if (j < n) {
-        const float p = s[j];
-        const float* vr = stage + lane * 32;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 f = lds_f4(vr + ((c ^ (lane & 7)) << 2));
-          acc[4 * c] = __fadd_rn(acc[4 * c], __fmul_rn(p, f.x));
-          acc[4 * c + 1] = __fadd_rn(acc[4 * c + 1], __fmul_rn(p, f.y));
-          acc[4 * c + 2] = __fadd_rn(acc[4 * c + 2], __fmul_rn(p, f.z));
-          acc[4 * c + 3] = __fadd_rn(acc[4 * c + 3], __fmul_rn(p, f.w));
-        }
-      }
-      __syncwarp();
+  // Context: lane owns columns lane and lane + 32 and walks the keys in
+  // ascending order through the staged 32-key chunks (swizzled rows).
+  const int ga = lane >> 2, gb = 8 + (lane >> 2), e4 = lane & 3;
+  float acc_a = 0.0f, acc_b = 0.0f;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    if (c0 != 0) stage_rows64(stage, c0, n, vp, lane);
+    cp_async_wait_warp();
+    const int nk = min(32, n - c0);
+    for (int jr = 0; jr < nk; ++jr) {
+      const float p = s[c0 + jr];
+      const float* vr = stage + jr * 64;
+      acc_a = __fadd_rn(acc_a, __fmul_rn(p, vr[((ga ^ (jr & 15)) << 2) + e4]));
+      acc_b = __fadd_rn(acc_b, __fmul_rn(p, vr[((gb ^ (jr & 15)) << 2) + e4]));
     }
-    out[32 * cc + lane] = reduce_scatter32(acc);
+    __syncwarp();
   }
+  out[lane] = acc_a;
+  out[32 + lane] = acc_b;
   __syncwarp();
 }
 
