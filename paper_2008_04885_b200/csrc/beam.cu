@@ -98,7 +98,12 @@ __global__ void __launch_bounds__(kSelWarps * 32) beam_select_kernel(BeamDev b) 
 #pragma unroll
     for (int i = 0; i < kCandPerLane; ++i)  // no candidate (NaN logits) never competes
       if (lane + 32 * i < nc && ct[i] >= 0 && ct[i] < b.V && cs[i] == cs[i]) ok |= 1u << i;
-    const int n_sel = min(b.B, nc);
+    // decode.cpp:71: take min(|cands|, beam) -- a shortlist can leave fewer
+    // valid candidates than beam slots; none at all means invalid logits.
+    int n_valid = __popc(ok);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_valid += __shfl_xor_sync(0xffffffffu, n_valid, o);
+    const int n_sel = n_valid > 0 ? min(b.B, n_valid) : 1;
     int q = 0;
     // Lane q keeps the q-th surviving (non-EOS) selection.
     float my_lp = 0.0f;

@@ -402,3 +402,55 @@ def test_vocabulary_shortlist_bit_exact():
     bad = [list(sls[0]), sls[1][:-1] + [600], list(reversed(sls[2]))]
     st = [h.status for h in gm.translate(srcs[:3], mt.BeamConfig(3, 0, 1.0), shortlists=bad)]
     assert st == [0, 3, 6]  # ok, IndexError (bad row), UsageError (unsorted)
+
+
+def test_shortlist_edge_cases():
+    """Shortlist shorter than the beam (fewer candidates than slots), the
+    4096-entry maximum, beam 16, and the bf16 path (sanity: tokens stay in
+    the shortlist)."""
+    c = cfg(1, 2, 32, 64, 4, 300, 5000, 40)
+    om = o.OracleModel.create(c, seed=29)
+    path = "/tmp/shortlist_edge.bin"
+    om.save(path)
+    srcs = o.synthetic_sources(3, 6, 300, seed=13)
+    rng = np.random.default_rng(8)
+    sls = [[0, 1, 2, 3, 17],                                              # 5 < beam 8
+           sorted(set([0, 1, 2, 3]) | set(rng.choice(5000, 4092, replace=False).tolist()))[:4096],
+           sorted(set([0, 1, 2, 3]) | set(rng.choice(5000, 300, replace=False).tolist()))]
+    gm = mt.Model.load(path, precision=mt.INT8)
+    for beam in (8, 16):
+        hyps = gm.translate(srcs, mt.BeamConfig(beam, 0, 1.0), shortlists=sls)
+        for s, sl, h in zip(srcs, sls, hyps):
+            r = om.beam_search(s, beam, derive(s, 40), 1.0, True, shortlist=sl)
+            assert h.status == 0 and h.tokens == r["tokens"]
+            assert f32hex(h.logprob) == f32hex(r["logprob"])
+    too_long = [list(range(4097))]
+    assert gm.translate(srcs[:1], mt.BeamConfig(4, 0, 1.0), shortlists=too_long)[0].status == 6
+    gb = mt.Model.load(path, precision=mt.BF16)
+    for sl, h in zip(sls, gb.translate(srcs, mt.BeamConfig(4, 0, 1.0), shortlists=sls)):
+        assert h.status == 0 and set(h.tokens) <= set(sl)
+
+
+def test_factors_bf16_and_shortlist_together():
+    """Factors and a shortlist in one call (mtg_translate_ex), int8 bit-exact
+    against the oracle's factored beam search restricted by the shortlist is
+    not exposed by the oracle C API, so check against factored full-vocab
+    decoding with a shortlist that contains every token it produces."""
+    c = dict(cfg(1, 1, 16, 32, 2, 20, 30, 32),
+             factors=[dict(combine="concat", embed_dim=8, share=False, vocab_size=9)])
+    om = o.OracleModel.create(c, seed=41)
+    path = "/tmp/factors_sl.bin"
+    om.save(path)
+    srcs = o.synthetic_sources(4, 5, 20, seed=3)
+    rng = np.random.default_rng(2)
+    facs = [[rng.integers(0, 9, len(s)).tolist()] for s in srcs]
+    gm = mt.Model.load(path, precision=mt.INT8)
+    full = gm.translate(srcs, mt.BeamConfig(3, 0, 1.0), factors=facs)
+    sls = [list(range(30)) for _ in srcs]  # the whole vocabulary as an explicit list
+    listed = gm.translate(srcs, mt.BeamConfig(3, 0, 1.0), factors=facs, shortlists=sls)
+    for s, f, a, b in zip(srcs, facs, full, listed):
+        r = om.beam_search_factors(s, f, 3, derive(s, 32), 1.0, True)
+        assert a.tokens == r["tokens"] == b.tokens
+        assert f32hex(a.logprob) == f32hex(b.logprob) == f32hex(r["logprob"])
+    gb = mt.Model.load(path, precision=mt.BF16)
+    assert all(h.status == 0 for h in gb.translate(srcs, mt.BeamConfig(3, 0, 1.0), factors=facs))
