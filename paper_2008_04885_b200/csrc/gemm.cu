@@ -49,11 +49,11 @@ CUtensorMap make_map(const void* ptr, int prec, int rows, int k_pad, int box_row
   return m;
 }
 
-template <int PREC, int BN, int EPI>
+template <int PREC, int BN, int EPI, int FL = -1>
 void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN, EPI>,
+    MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN, EPI, FL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
@@ -73,11 +73,11 @@ void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) 
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    MTG_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<PREC, BN, EPI>, p.a, p.b, p.a2, p.b2,
+    MTG_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<PREC, BN, EPI, FL>, p.a, p.b, p.a2, p.b2,
                                 p.num_kb, p.nst, ep));
   } else {
-    launch_k(gemm_tc_kernel<PREC, BN, EPI>, grid, kGemmThreads, p.smem, stream, p.a, p.b, p.a2,
-             p.b2, p.num_kb, p.nst, ep);
+    launch_k(gemm_tc_kernel<PREC, BN, EPI, FL>, grid, kGemmThreads, p.smem, stream, p.a, p.b,
+             p.a2, p.b2, p.num_kb, p.nst, ep);
   }
   MTG_CUDA(cudaGetLastError());
 }
@@ -114,6 +114,19 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
       case 64: return launch_one<PREC, 64, kEpiSegMax>(p, ep, stream);
       case 128: return launch_one<PREC, 128, kEpiSegMax>(p, ep, stream);
       case 256: return launch_one<PREC, 256, kEpiSegMax>(p, ep, stream);
+    }
+  }
+  // The decoder GEMMs' options fixed at compile time (BN = 32; measured
+  // +1.5 % int8; the same for the encoder's BN = 128 GEMMs was neutral).
+  const int fl = (ep.bias ? 1 : 0) | (ep.relu ? 2 : 0) | (ep.residual ? 4 : 0) |
+                 (ep.d_step ? 8 : 0);
+  if (p.bn == 32) {
+    switch (fl) {
+      case 0: return launch_one<PREC, 32, kEpiLinear, 0>(p, ep, stream);
+      case 3: return launch_one<PREC, 32, kEpiLinear, 3>(p, ep, stream);
+      case 4: return launch_one<PREC, 32, kEpiLinear, 4>(p, ep, stream);
+      case 5: return launch_one<PREC, 32, kEpiLinear, 5>(p, ep, stream);
+      case 8: return launch_one<PREC, 32, kEpiLinear, 8>(p, ep, stream);
     }
   }
   switch (p.bn) {

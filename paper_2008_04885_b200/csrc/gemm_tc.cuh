@@ -111,7 +111,10 @@ __host__ __device__ constexpr int gemm_tmem_cols(int bn) {
 constexpr int kGemmSmemExtra = 1024 /*align*/ + 256 /*barriers*/;
 constexpr int kEpiStageBytes = kEpiWarps * 32 * 33 * 4;  // aliases the drained pipeline
 
-template <int PREC, int BN, int EPI>
+// FL >= 0 fixes the epilogue options at compile time (bit 0 bias, 1 ReLU,
+// 2 residual, 3 step offset) -- the hot small GEMMs measure faster with no
+// runtime option checks; FL = -1 reads them from the GemmEpilogue.
+template <int PREC, int BN, int EPI, int FL = -1>
 __global__ void __launch_bounds__(kGemmThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB,
@@ -318,10 +321,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         inv[s] = c0 < ep.N ? __frcp_rn(__fmul_rn(sa, ep.w_seg_scale[s])) : 1.0f;
       }
     }
+    const bool has_step = FL >= 0 ? (FL & 8) != 0 : ep.d_step != nullptr;
     const long long step_off =
-        ep.d_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride : 0LL;
-    const bool has_bias = ep.bias != nullptr, has_res = ep.residual != nullptr;
-    const bool relu = ep.relu != 0;
+        has_step ? static_cast<long long>(*ep.d_step) * ep.c_step_stride : 0LL;
+    const bool has_bias = FL >= 0 ? (FL & 1) != 0 : ep.bias != nullptr;
+    const bool has_res = FL >= 0 ? (FL & 4) != 0 : ep.residual != nullptr;
+    const bool relu = FL >= 0 ? (FL & 2) != 0 : ep.relu != 0;
     constexpr bool seg_mode = EPI == kEpiSegMax;  // host: no residual
     float seg_max = 0.0f;
     int seg_bad = 0;
