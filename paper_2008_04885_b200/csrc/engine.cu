@@ -282,9 +282,18 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   n_sent = std::max(n_sent, 1);
   m_enc = std::max(m_enc, 1);
   beam = std::max(beam, 1);
-  if (n_sent <= cap_sent_ && m_enc <= cap_enc_ && beam <= cap_beam_) return;
-  cap_sent_ = std::max(n_sent, cap_sent_);
-  cap_enc_ = std::max(m_enc, cap_enc_);
+  // Grids, GEMM plans (split-K, tile widths) and the step graph are sized by
+  // the capacity, so a much smaller batch after a big one (batch-1 serving)
+  // shrinks the workspace instead of running mostly-idle grids.
+  const bool shrink = cap_sent_ > 0 && 8 * n_sent <= cap_sent_ && 8 * m_enc <= cap_enc_;
+  if (!shrink && n_sent <= cap_sent_ && m_enc <= cap_enc_ && beam <= cap_beam_) return;
+  if (shrink) {
+    cap_sent_ = n_sent;
+    cap_enc_ = m_enc;
+  } else {
+    cap_sent_ = std::max(n_sent, cap_sent_);
+    cap_enc_ = std::max(m_enc, cap_enc_);
+  }
   cap_beam_ = std::max(beam, cap_beam_);
   plan_cache(this).clear();
   ++ws_gen_;

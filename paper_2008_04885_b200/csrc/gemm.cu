@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -167,11 +168,25 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   // Split-K over a z cluster when the output tiles cannot fill the SMs and a
   // tile's K stream is long (the DSMEM reduction costs ~1 us): aim for
   // >= ~160 KB of operand bytes per split, at most 8 (portable cluster).
+  // MTG_SPLIT_CTAS / MTG_SPLIT_KB override the target grid size and bytes
+  // per split (A/B experiments); default 160 KB per split.
+  // Single-m-tile GEMMs (batch-1 decoding) are pure latency: aim for two
+  // CTAs per SM there (measured: fp32 p90 batch-1 -9 %); one per SM otherwise
+  // (batch-64 throughput drops with more splits).
+  static const int split_ctas_env = [] {
+    const char* e = std::getenv("MTG_SPLIT_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int split_ctas = split_ctas_env > 0 ? split_ctas_env : (p.m_tiles == 1 ? 296 : 148);
+  static const long long split_bytes = [] {
+    const char* e = std::getenv("MTG_SPLIT_KB");
+    return (e ? std::atoll(e) : 160LL) * 1024;
+  }();
   const int tiles = p.m_tiles * p.n_tiles;
   const long long tile_bytes = static_cast<long long>(p.num_kb) * gemm_stage_bytes(a.prec, bn);
-  const int by_bytes = static_cast<int>((tile_bytes + 160 * 1024 - 1) / (160 * 1024));
+  const int by_bytes = static_cast<int>((tile_bytes + split_bytes - 1) / split_bytes);
   if (allow_split && tiles < 148 && p.num_kb >= 4 && by_bytes > 1)
-    p.splits = std::max(1, std::min({p.num_kb / 2, 148 / tiles, 8, by_bytes}));
+    p.splits = std::max(1, std::min({p.num_kb / 2, split_ctas / tiles, 8, by_bytes}));
   // Pipeline depth: no deeper than the K loop, and shallow enough for two
   // CTAs per SM when the tile allows it (epilogue / mainloop overlap, and the
   // next kernel's CTAs can start under PDL; measured: a one-CTA-per-SM depth
