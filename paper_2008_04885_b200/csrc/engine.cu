@@ -195,6 +195,7 @@ Engine::Engine(HostModel model, int precision, int device)
 Engine::~Engine() {
   cudaSetDevice(device_);
   diag_clear();
+  clear_enc_graphs();
   plan_cache(this).clear();
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);
@@ -296,6 +297,7 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   }
   cap_beam_ = std::max(beam, cap_beam_);
   plan_cache(this).clear();
+  clear_enc_graphs();
   ++ws_gen_;
   const ModelConfig& c = host_.config;
   const int N = cap_sent_, M = cap_enc_, B = cap_beam_;
@@ -709,6 +711,42 @@ void Engine::run_encoder(int n_sent, int m, int max_src) {
     MTG_CUDA(cudaEventCreate(&enc_marks_.back().ev));
     MTG_CUDA(cudaEventRecord(enc_marks_.back().ev, stream_));
   }
+  static const bool graphs = [] {
+    const char* e = std::getenv("MTG_ENC_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  if (graphs && !diag_ && !capturing_) {
+    // The encoder's ~9 kernels per layer replay as one CUDA graph per batch
+    // shape (exact key: workspace generation, sizes, factor-id buffer).
+    const EncKey key{ws_gen_, n_sent, m, max_src, src_fids_.get()};
+    auto it = enc_graphs_.find(key);
+    if (it == enc_graphs_.end()) {
+      if (enc_graphs_.size() >= 256) clear_enc_graphs();
+      const int64_t before = launches_;
+      cudaGraph_t g = nullptr;
+      MTG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      capturing_ = true;
+      try {
+        run_encoder_body(n_sent, m, max_src);
+      } catch (...) {
+        capturing_ = false;
+        cudaStreamEndCapture(stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      capturing_ = false;
+      MTG_CUDA(cudaStreamEndCapture(stream_, &g));
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t err = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      MTG_CUDA(err);
+      it = enc_graphs_.emplace(key, std::make_pair(exec, launches_ - before)).first;
+      launches_ = before;
+    }
+    MTG_CUDA(cudaGraphLaunch(it->second.first, stream_));
+    launches_ += it->second.second;
+    return;
+  }
   run_encoder_body(n_sent, m, max_src);
   if (enc_diag_active_) {
     enc_diag_active_ = false;
@@ -725,6 +763,11 @@ void Engine::run_encoder(int n_sent, int m, int max_src) {
     enc_marks_.clear();
     ++enc_runs_;
   }
+}
+
+void Engine::clear_enc_graphs() {
+  for (auto& kv : enc_graphs_) cudaGraphExecDestroy(kv.second.first);
+  enc_graphs_.clear();
 }
 
 void Engine::run_encoder_body(int n_sent, int m, int max_src) {

@@ -7,6 +7,7 @@
 #include <memory>
 #include <mutex>
 #include <map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -215,6 +216,15 @@ class Engine {
   // One decode step (decoder layers, logits, top-k, beam bookkeeping) as a
   // CUDA graph, re-captured when the batch shape / beam / alpha changes.
   void ensure_step_graph();
+  struct EncKey {
+    int gen, n, m, max_src;
+    const void* fids;
+    bool operator<(const EncKey& o) const {
+      return std::tie(gen, n, m, max_src, fids) < std::tie(o.gen, o.n, o.m, o.max_src, o.fids);
+    }
+  };
+  std::map<EncKey, std::pair<cudaGraphExec_t, int64_t>> enc_graphs_;
+  void clear_enc_graphs();
   cudaGraph_t step_graph_ = nullptr;
   cudaGraphExec_t step_exec_ = nullptr;
   int64_t step_kernels_ = 0;
