@@ -987,17 +987,30 @@ void Engine::ensure_step_graph() {
       MTG_CUDA(cudaEventRecordWithFlags(diag_marks_.back().ev, stream_, cudaEventRecordExternal));
     }
     decoder_body(true);
-    if (use_shortlist_) {
-      launch_shortlist_topk(prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2, shortlist_args(), beam_,
-                            stream_);
-      count("shortlist logits + softmax + top-k");
+    // Step tail: top-k of every live row + per-sentence selection, fused into
+    // one kernel by default (MTG_FUSED_TAIL=0: two kernels, A/B).
+    static const bool fused_tail = [] {
+      const char* e = std::getenv("MTG_FUSED_TAIL");
+      return !(e && e[0] == '0');
+    }();
+    const int sl_prec = prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2;
+    const ShortlistArgs sla = shortlist_args();
+    if (fused_tail && beam_.N >= 8) {  // measured: neutral-to-worse for batch-1
+      launch_topk_select(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
+                         part_ld_, use_shortlist_ ? &sla : nullptr, sl_prec, beam_, stream_);
+      count("top-k + beam select");
     } else {
-      launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
-                          part_ld_, beam_, stream_);
-      count("softmax + top-k merge");
+      if (use_shortlist_) {
+        launch_shortlist_topk(sl_prec, sla, beam_, stream_);
+        count("shortlist logits + softmax + top-k");
+      } else {
+        launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
+                            part_ld_, beam_, stream_);
+        count("softmax + top-k merge");
+      }
+      launch_beam_select(beam_, stream_);
+      count("beam select");
     }
-    launch_beam_select(beam_, stream_);
-    count("beam select");
   } catch (...) {
     capturing_ = false;
     cudaGraph_t g = nullptr;

@@ -194,6 +194,12 @@ struct ShortlistArgs {
   const float* wf = nullptr;
 };
 void launch_shortlist_topk(int prec, const ShortlistArgs& a, const BeamDev& b, cudaStream_t st);
+// Fused step tail (topk.cu): per-sentence CTA running the top-k of its rows
+// (full vocabulary from the projection partials, or the shortlist when sa is
+// set) and then the beam selection + compaction of launch_beam_select.
+void launch_topk_select(const float* logits, long long ldl, const float* part_m,
+                        const float* part_s, const int* part_arg, long long part_ld,
+                        const ShortlistArgs* sa, int prec, const BeamDev& b, cudaStream_t st);
 void launch_softmax_topk(const float* logits, long long ldl, const float* part_m,
                          const float* part_s, const int* part_arg, long long part_ld,
                          const BeamDev& b, cudaStream_t st);

@@ -17,8 +17,12 @@
 // score(m_k) >= S_kB scores < S_kB and ranks below kB slice maxima, so the
 // exact top-kB lies in those slices -- normally exactly kB of them -- which
 // are rescanned from the logits the GEMM wrote.
+#include <algorithm>
 #include <climits>
+#include <map>
+#include <mutex>
 
+#include "beam_dev.cuh"
 #include "detmath.cuh"
 #include "errors.hpp"
 #include "kernels.cuh"
@@ -51,15 +55,21 @@ __device__ __forceinline__ void warp_best(float& bs, int& bt) {
   }
 }
 
-// CTA-wide (4 warps) argmax; every thread gets the winner.
-__device__ __forceinline__ void block_best(float& bs, int& bt, float* rf, int* ri) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Barrier of one 128-thread group (id 0 with a 128-thread CTA == __syncthreads).
+__device__ __forceinline__ void grp_sync(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+// Group-wide (4 warps) argmax; every thread gets the winner. tid: 0..127.
+__device__ __forceinline__ void block_best(float& bs, int& bt, float* rf, int* ri, int tid,
+                                           int bar) {
+  const int lane = tid & 31, warp = tid >> 5;
   warp_best(bs, bt);
   if (lane == 0) {
     rf[warp] = bs;
     ri[warp] = bt;
   }
-  __syncthreads();
+  grp_sync(bar);
   bs = rf[0];
   bt = ri[0];
 #pragma unroll
@@ -68,26 +78,31 @@ __device__ __forceinline__ void block_best(float& bs, int& bt, float* rf, int* r
       bs = rf[w];
       bt = ri[w];
     }
-  __syncthreads();
+  grp_sync(bar);
 }
+
+// Per-group shared scratch of the row routines.
+struct RowScratch {
+  float red_f[kMT / 32];
+  int red_i[kMT / 32];
+  int n_list;
+  int list[kMaxShortlist];  // rescan list (merge) or shortlist logits (shortlist)
+};
 
 // One CTA (128 threads) per live hypothesis row; thread t owns slices
 // t + 128 i. Sum order P6: thread partials in i order, P1 butterfly per warp,
 // then (W0 + W1) + (W2 + W3).
-__global__ void __launch_bounds__(kMT)
-    softmax_topk_kernel(const float* __restrict__ logits, long long ldl,
-                        const float* __restrict__ part_m, const float* __restrict__ part_s,
-                        const int* __restrict__ part_arg, long long part_ld, int nsub,
-                        BeamDev b) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ float red_f[kMT / 32];
-  __shared__ int red_i[kMT / 32];
-  __shared__ int list_s[kMaxSoftmaxSlices];
-  __shared__ int n_list_s;
-  const int r = blockIdx.x;
-  if (r >= *b.n_rows) return;  // uniform over the CTA
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ void merge_row(int r, const float* __restrict__ logits, long long ldl,
+                                      const float* __restrict__ part_m,
+                                      const float* __restrict__ part_s,
+                                      const int* __restrict__ part_arg, long long part_ld,
+                                      int nsub, const BeamDev& b, int tid, int bar,
+                                      RowScratch& sc_) {
+  float* red_f = sc_.red_f;
+  int* red_i = sc_.red_i;
+  int* list_s = sc_.list;
+  int& n_list_s = sc_.n_list;
+  const int lane = tid & 31, warp = tid >> 5;
   const int V = b.V;
   const int kB = min(b.B, V);
   const float* pm = part_m + r * part_ld;
@@ -113,9 +128,9 @@ __global__ void __launch_bounds__(kMT)
   for (int i = 0; i < kSubPerThread; ++i) mloc = fmaxf(mloc, mv[i]);
   mloc = warp_allmax(mloc);
   if (lane == 0) red_f[warp] = mloc;
-  __syncthreads();
+  grp_sync(bar);
   const float M = fmaxf(fmaxf(red_f[0], red_f[1]), fmaxf(red_f[2], red_f[3]));
-  __syncthreads();
+  grp_sync(bar);
   float part = 0.0f;
 #pragma unroll
   for (int i = 0; i < kSubPerThread; ++i) {
@@ -127,9 +142,9 @@ __global__ void __launch_bounds__(kMT)
   }
   part = warp_allsum(part);
   if (lane == 0) red_f[warp] = part;
-  __syncthreads();
+  grp_sync(bar);
   const float total = __fadd_rn(__fadd_rn(red_f[0], red_f[1]), __fadd_rn(red_f[2], red_f[3]));
-  __syncthreads();
+  grp_sync(bar);
   const float lse = __fadd_rn(det_logf(total), M);
 
   // Slice-max scores; a slice with no max (all NaN / empty) never competes.
@@ -153,7 +168,7 @@ __global__ void __launch_bounds__(kMT)
         bs = sc[i];
         bt = at[i];
       }
-    block_best(bs, bt, red_f, red_i);
+    block_best(bs, bt, red_f, red_i, tid, bar);
     if (bt == INT_MAX) {  // fewer than kB slices: every valid slice is rescanned
       thr = kNegInf;
       break;
@@ -166,7 +181,7 @@ __global__ void __launch_bounds__(kMT)
 #pragma unroll
   for (int i = 0; i < kSubPerThread; ++i)
     if (at[i] >= 0 && sc[i] >= thr) list_s[atomicAdd(&n_list_s, 1)] = tid + kMT * i;
-  __syncthreads();
+  grp_sync(bar);
   const int n_list = n_list_s;
   // Exact top-kB over the rescanned slices: warp w takes list entries
   // w, w + 4, ...; lane = column within the slice.
@@ -206,7 +221,7 @@ __global__ void __launch_bounds__(kMT)
         }
       }
     }
-    block_best(bs, bt, red_f, red_i);
+    block_best(bs, bt, red_f, red_i, tid, bar);
     if (tid == 0) {
       b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
       b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
@@ -222,6 +237,18 @@ __global__ void __launch_bounds__(kMT)
   }
 }
 
+__global__ void __launch_bounds__(kMT)
+    softmax_topk_kernel(const float* __restrict__ logits, long long ldl,
+                        const float* __restrict__ part_m, const float* __restrict__ part_s,
+                        const int* __restrict__ part_arg, long long part_ld, int nsub,
+                        BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ RowScratch sc;
+  const int r = blockIdx.x;
+  if (r >= *b.n_rows) return;  // uniform over the CTA
+  merge_row(r, logits, ldl, part_m, part_s, part_arg, part_ld, nsub, b, threadIdx.x, 0, sc);
+}
 
 // ---- vocabulary shortlist (decode.cpp:55-61 with rows; model.cpp:440-449) ----
 // One 128-thread CTA per live row r of sentence s with shortlist L_s (sorted
@@ -235,15 +262,12 @@ __global__ void __launch_bounds__(kMT)
 //          (the oracle's dot8 stand-in for Eigen's dot, tensor.cpp:125-133).
 //   bf16 : bf16 operands, products summed in fp32 in k order.
 template <int PREC>
-__global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, BeamDev b) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ float lg[kMaxShortlist];
-  __shared__ float red_f[kMT / 32];
-  __shared__ int red_i[kMT / 32];
-  const int r = blockIdx.x;
-  if (r >= *b.n_rows) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ void shortlist_row(int r, const ShortlistArgs& a, const BeamDev& b,
+                                          int tid, int bar, RowScratch& sc_) {
+  float* lg = reinterpret_cast<float*>(sc_.list);  // kMaxShortlist floats
+  float* red_f = sc_.red_f;
+  int* red_i = sc_.red_i;
+  const int lane = tid & 31, warp = tid >> 5;
   const int s = b.row_sent[r];
   const int* ids = a.sl_ids + a.sl_off[s];
   const int n = a.sl_off[s + 1] - a.sl_off[s];
@@ -287,7 +311,7 @@ __global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, Be
     }
     lg[j] = x;
   }
-  __syncthreads();
+  grp_sync(bar);
   // log-sum-exp in the P6 order over the n subset positions.
   const int nsub = (n + 31) / 32;
   float mloc = kNegInf;
@@ -317,9 +341,9 @@ __global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, Be
   }
   mloc = warp_allmax(mloc);
   if (lane == 0) red_f[warp] = mloc;
-  __syncthreads();
+  grp_sync(bar);
   const float M = fmaxf(fmaxf(red_f[0], red_f[1]), fmaxf(red_f[2], red_f[3]));
-  __syncthreads();
+  grp_sync(bar);
   float part = 0.0f;
 #pragma unroll
   for (int i = 0; i < kMaxShortlist / 32 / kMT + 1; ++i)
@@ -330,9 +354,9 @@ __global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, Be
     }
   part = warp_allsum(part);
   if (lane == 0) red_f[warp] = part;
-  __syncthreads();
+  grp_sync(bar);
   const float total = __fadd_rn(__fadd_rn(red_f[0], red_f[1]), __fadd_rn(red_f[2], red_f[3]));
-  __syncthreads();
+  grp_sync(bar);
   const float lse = __fadd_rn(det_logf(total), M);
   // Top-kB by (score desc, token asc), token = ids[j].
   const int kB = min(b.B, n);
@@ -349,7 +373,7 @@ __global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, Be
         bt = tk;
       }
     }
-    block_best(bs, bt, red_f, red_i);
+    block_best(bs, bt, red_f, red_i, tid, bar);
     if (tid == 0) {
       b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
       b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
@@ -364,6 +388,60 @@ __global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, Be
   }
 }
 
+template <int PREC>
+__global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ RowScratch sc;
+  const int r = blockIdx.x;
+  if (r >= *b.n_rows) return;
+  shortlist_row<PREC>(r, a, b, threadIdx.x, 0, sc);
+}
+
+// ---- fused step tail --------------------------------------------------------
+// One CTA per sentence: G = blockDim / 128 groups each run merge_row (or
+// shortlist_row) for the sentence's live rows, then warp 0 runs the
+// sentence's beam selection from those candidates and the last CTA compacts
+// the rows (beam_dev.cuh) -- the work of softmax_topk_kernel +
+// beam_select_kernel without the kernel boundary between them.
+struct TailArgs {
+  const float* logits;
+  long long ldl;
+  const float* part_m;
+  const float* part_s;
+  const int* part_arg;
+  long long part_ld;
+  int nsub;
+};
+
+template <int MODE>  // 0 full vocabulary; 1..3 shortlist with PREC = MODE - 1
+__global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, ShortlistArgs sa,
+                                                           BeamDev b) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) unsigned char tail_smem[];
+  const int G = blockDim.x / kMT, g = threadIdx.x / kMT, tid = threadIdx.x % kMT;
+  RowScratch* scr = reinterpret_cast<RowScratch*>(tail_smem);
+  int* live_s = reinterpret_cast<int*>(scr + G);
+  int* row0_s = live_s + b.N;
+  __shared__ int is_last;
+  const int s = blockIdx.x;
+  const int t = *b.step;
+  if (!b.sent_done[s]) {
+    const int L = b.sent_live[s], r0 = b.sent_row0[s];
+    for (int i = g; i < L; i += G) {
+      if constexpr (MODE == 0)
+        merge_row(r0 + i, ta.logits, ta.ldl, ta.part_m, ta.part_s, ta.part_arg, ta.part_ld,
+                  ta.nsub, b, tid, 1 + g, scr[g]);
+      else
+        shortlist_row<MODE - 1>(r0 + i, sa, b, tid, 1 + g, scr[g]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) select_sentence(b, s, t, threadIdx.x);
+  finish_select(b, t, live_s, row0_s, &is_last);
+}
+
 }  // namespace
 
 long long topk_pitch(int V) {
@@ -372,6 +450,39 @@ long long topk_pitch(int V) {
 }
 
 long long softmax_part_pitch(int V) { return ((V + 31) / 32 + 3) / 4 * 4; }
+
+void launch_topk_select(const float* logits, long long ldl, const float* part_m,
+                        const float* part_s, const int* part_arg, long long part_ld,
+                        const ShortlistArgs* sa, int prec, const BeamDev& b, cudaStream_t st) {
+  if (b.B > kMaxBeam) fail(kUsageError, "beam size above 16 is not supported");
+  const int nsub = (b.V + 31) / 32;
+  if (!sa && nsub > kMaxSoftmaxSlices)
+    fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
+  const int G = std::min(b.B, 8);
+  const size_t smem = sizeof(RowScratch) * G + sizeof(int) * 2 * static_cast<size_t>(b.N);
+  if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
+  TailArgs ta{logits, ldl, part_m, part_s, part_arg, part_ld, nsub};
+  const ShortlistArgs none{};
+  auto launch = [&](auto kern) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> configured;  // per kernel instantiation
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      size_t& c = configured[reinterpret_cast<const void*>(kern)];
+      if (smem > 48 * 1024 && smem > c) {
+        MTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        c = smem;
+      }
+    }
+    launch_k(kern, b.N, kMT * G, smem, st, ta, sa ? *sa : none, b);
+  };
+  if (!sa) launch(topk_select_kernel<0>);
+  else if (prec == 0) launch(topk_select_kernel<1>);
+  else if (prec == 1) launch(topk_select_kernel<2>);
+  else launch(topk_select_kernel<3>);
+  MTG_CUDA(cudaGetLastError());
+}
 
 void launch_shortlist_topk(int prec, const ShortlistArgs& a, const BeamDev& b, cudaStream_t st) {
   if (b.B > kMaxBeam) fail(kUsageError, "beam size above 16 is not supported");

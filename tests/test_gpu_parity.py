@@ -322,15 +322,18 @@ def test_step_fusion_modes_agree():
         "c = dict(num_encoder_layers=2, num_decoder_layers=2, d_model=64, d_ff=256, num_heads=4,"
         " src_vocab_size=700, tgt_vocab_size=900, dropout=0.0, max_seq_len=64)\n"
         "gm = mt.Model.create(c, seed=3, precision=mt.INT8)\n"
-        "srcs = o.synthetic_sources(6, 9, 700, seed=2)\n"
+        "srcs = o.synthetic_sources(12, 9, 700, seed=2)\n"
         "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs, mt.BeamConfig(5, 0, 1.0))])\n"
     ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for mode in ("0", "1", "2"):
-        env = dict(os.environ, MTG_STEP_FUSION=mode)
+    variants = [dict(MTG_STEP_FUSION="0"), dict(MTG_STEP_FUSION="1"), dict(MTG_STEP_FUSION="2"),
+                dict(MTG_FUSED_TAIL="0"), dict(MTG_LOGITS_PERSISTENT="1"),
+                dict(MTG_NO_SPLIT_K="1"), dict(MTG_ENC_GRAPH="0"), dict(MTG_NO_ENC_FUSION="1")]
+    for v in variants:  # every A/B switch must leave the bits unchanged
+        env = dict(os.environ, **v)
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
                                    capture_output=True, text=True).stdout)
-    assert outs[0] == outs[1] == outs[2] and outs[0].strip()
+    assert outs[0].strip() and all(o == outs[0] for o in outs)
 
 
 @pytest.mark.parametrize("combine,shared", [("concat", False), ("sum", False), ("average", True),
