@@ -21,6 +21,7 @@
 #include <climits>
 #include <map>
 #include <mutex>
+#include <type_traits>
 
 #include "beam_dev.cuh"
 #include "detmath.cuh"
@@ -81,13 +82,17 @@ __device__ __forceinline__ void block_best(float& bs, int& bt, float* rf, int* r
   grp_sync(bar);
 }
 
-// Per-group shared scratch of the row routines.
-struct RowScratch {
+// Per-group shared scratch of the row routines: CAP ints of rescan list
+// (merge, kMaxSoftmaxSlices) or shortlist logits (kMaxShortlist).
+template <int CAP>
+struct RowScratchT {
   float red_f[kMT / 32];
   int red_i[kMT / 32];
   int n_list;
-  int list[kMaxShortlist];  // rescan list (merge) or shortlist logits (shortlist)
+  int list[CAP];
 };
+using MergeScratch = RowScratchT<kMaxSoftmaxSlices>;
+using ShortlistScratch = RowScratchT<kMaxShortlist>;
 
 // One CTA (128 threads) per live hypothesis row; thread t owns slices
 // t + 128 i. Sum order P6: thread partials in i order, P1 butterfly per warp,
@@ -97,7 +102,7 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
                                       const float* __restrict__ part_s,
                                       const int* __restrict__ part_arg, long long part_ld,
                                       int nsub, const BeamDev& b, int tid, int bar,
-                                      RowScratch& sc_) {
+                                      MergeScratch& sc_) {
   float* red_f = sc_.red_f;
   int* red_i = sc_.red_i;
   int* list_s = sc_.list;
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(kMT)
                         BeamDev b) {
   pdl_wait();
   pdl_trigger();
-  __shared__ RowScratch sc;
+  __shared__ MergeScratch sc;
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;  // uniform over the CTA
   merge_row(r, logits, ldl, part_m, part_s, part_arg, part_ld, nsub, b, threadIdx.x, 0, sc);
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(kMT)
 //   bf16 : bf16 operands, products summed in fp32 in k order.
 template <int PREC>
 __device__ __forceinline__ void shortlist_row(int r, const ShortlistArgs& a, const BeamDev& b,
-                                          int tid, int bar, RowScratch& sc_) {
+                                          int tid, int bar, ShortlistScratch& sc_) {
   float* lg = reinterpret_cast<float*>(sc_.list);  // kMaxShortlist floats
   float* red_f = sc_.red_f;
   int* red_i = sc_.red_i;
@@ -392,7 +397,7 @@ template <int PREC>
 __global__ void __launch_bounds__(kMT) shortlist_topk_kernel(ShortlistArgs a, BeamDev b) {
   pdl_wait();
   pdl_trigger();
-  __shared__ RowScratch sc;
+  __shared__ ShortlistScratch sc;
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;
   shortlist_row<PREC>(r, a, b, threadIdx.x, 0, sc);
@@ -421,7 +426,8 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char tail_smem[];
   const int G = blockDim.x / kMT, g = threadIdx.x / kMT, tid = threadIdx.x % kMT;
-  RowScratch* scr = reinterpret_cast<RowScratch*>(tail_smem);
+  using Scratch = std::conditional_t<MODE == 0, MergeScratch, ShortlistScratch>;
+  Scratch* scr = reinterpret_cast<Scratch*>(tail_smem);
   int* live_s = reinterpret_cast<int*>(scr + G);
   int* row0_s = live_s + b.N;
   __shared__ int is_last;
@@ -459,7 +465,8 @@ void launch_topk_select(const float* logits, long long ldl, const float* part_m,
   if (!sa && nsub > kMaxSoftmaxSlices)
     fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
   const int G = std::min(b.B, 8);
-  const size_t smem = sizeof(RowScratch) * G + sizeof(int) * 2 * static_cast<size_t>(b.N);
+  const size_t smem = (sa ? sizeof(ShortlistScratch) : sizeof(MergeScratch)) * G +
+                      sizeof(int) * 2 * static_cast<size_t>(b.N);
   if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
   TailArgs ta{logits, ldl, part_m, part_s, part_arg, part_ld, nsub};
   const ShortlistArgs none{};
