@@ -63,6 +63,42 @@ __device__ __forceinline__ float det_expf_nonpos(float x) {
   return under ? 0.0f : (ni >= -125 ? fast : slow);
 }
 
+// det_expf_nonpos for x in [-86.5, 0] or NaN: same bits with fewer, full-rate
+// instructions. n = rint(x * log2e) via the 1.5 * 2^23 rounding add (round to
+// nearest even, like rintf), and 2^n (normal, n >= -125) is built from the
+// low bits of that sum, so no FRND / F2I and no subnormal path.
+__device__ __forceinline__ float det_expf_nonpos_fast(float x) {
+  const float t = __fadd_rn(__fmul_rn(x, 1.44269502162933349609375f), 12582912.0f);
+  const float n = __fsub_rn(t, 12582912.0f);
+  float r = __fmaf_rn(n, -0.693359375f, x);
+  r = __fmaf_rn(n, 2.12194440e-4f, r);
+  const float z = __fmul_rn(r, r);
+  float p = 1.9875691500e-4f;
+  p = __fmaf_rn(p, r, 1.3981999507e-3f);
+  p = __fmaf_rn(p, r, 8.3334519073e-3f);
+  p = __fmaf_rn(p, r, 4.1665795894e-2f);
+  p = __fmaf_rn(p, r, 1.6666665459e-1f);
+  p = __fmaf_rn(p, r, 5.0000001201e-1f);
+  p = __fmaf_rn(p, z, r);
+  p = __fadd_rn(p, 1.0f);
+  return __fmul_rn(p, __int_as_float((__float_as_int(t) << 23) + 0x3f800000));
+}
+
+// Sequential sum of exp(s[j] - best), j < nv, in column order (P6). `mn` is
+// the lane's fminf over its nv values; when every lane of the warp has
+// mn - best >= -86.5 the fast exp gives the same bits as det_expf_nonpos.
+__device__ __forceinline__ float det_sum_exp(const float* s, int nv, float best, float mn) {
+  float sum = 0.0f;
+  if (__all_sync(0xffffffffu, __fsub_rn(mn, best) >= -86.5f)) {
+#pragma unroll 4
+    for (int j = 0; j < nv; ++j) sum = __fadd_rn(sum, det_expf_nonpos_fast(__fsub_rn(s[j], best)));
+  } else {
+#pragma unroll 4
+    for (int j = 0; j < nv; ++j) sum = __fadd_rn(sum, det_expf_nonpos(__fsub_rn(s[j], best)));
+  }
+  return sum;
+}
+
 __device__ __forceinline__ float det_logf(float x) {
   if (x != x) return x;
   if (x < 0.0f) return __int_as_float(0x7fc00000);

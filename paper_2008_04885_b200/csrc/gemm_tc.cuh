@@ -466,19 +466,18 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         const int col0 = n0 + c;
         const int nv = min(kChunk, N - col0);
         float best = -__int_as_float(0x7f800000);
+        float mn = __int_as_float(0x7f800000);
         int bi = -1;
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
           const bool take = j < nv && v[j] > best;
           best = take ? v[j] : best;
           bi = take ? col0 + j : bi;
+          mn = j < nv ? fminf(mn, v[j]) : mn;
         }
-        float sum = 0.0f;
-        if (bi >= 0) {
-          const float* sv = stage + lane * 33;
-#pragma unroll 4
-          for (int j = 0; j < nv; ++j) sum = __fadd_rn(sum, det_expf_nonpos(__fsub_rn(sv[j], best)));
-        }
+        // all-NaN / all -inf slices: (best, sum, argmax) = (-inf, 0, -1)
+        const float sum =
+            det_sum_exp(stage + lane * 33, bi >= 0 ? nv : 0, best, bi >= 0 ? mn : 0.0f);
         const int k = (c - half * kHalf) / 32;
 #pragma unroll
         for (int kk = 0; kk < kSubs; ++kk)
