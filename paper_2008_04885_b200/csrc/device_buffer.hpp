@@ -18,24 +18,30 @@ class DeviceBuffer {
   ~DeviceBuffer() { release(); }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) {
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_), cap_(o.cap_) {
     o.p_ = nullptr;
-    o.n_ = 0;
+    o.n_ = o.cap_ = 0;
   }
   DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
     if (this != &o) {
       release();
       p_ = o.p_;
       n_ = o.n_;
+      cap_ = o.cap_;
       o.p_ = nullptr;
-      o.n_ = 0;
+      o.n_ = o.cap_ = 0;
     }
     return *this;
   }
 
-  // Reallocates (zero-filled) when n differs from the current size.
+  // Logical size n. Reallocates (zero-filled) only when n exceeds the
+  // allocation; shrinking keeps it, so the engine's workspace can follow the
+  // batch shape without cudaFree / cudaMalloc round trips. Contents are kept.
   void resize(size_t n) {
-    if (n == n_ && p_) return;
+    if (p_ && n <= cap_) {
+      n_ = n;
+      return;
+    }
     release();
     if (n) {
       MTG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
@@ -45,12 +51,12 @@ class DeviceBuffer {
       MTG_CUDA(cudaMemset(p_, 0, n * sizeof(T)));
       MTG_CUDA(cudaDeviceSynchronize());
     }
-    n_ = n;
+    n_ = cap_ = n;
   }
   void release() {
     if (p_) cudaFree(p_);
     p_ = nullptr;
-    n_ = 0;
+    n_ = cap_ = 0;
   }
   void upload(const T* host, size_t n, size_t offset = 0) {
     MTG_CUDA(cudaMemcpy(p_ + offset, host, n * sizeof(T), cudaMemcpyHostToDevice));
@@ -77,6 +83,7 @@ class DeviceBuffer {
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
+  size_t cap_ = 0;
 };
 
 }  // namespace mtg

@@ -161,7 +161,11 @@ Operand ActOperand::op() const {
 
 static std::map<PlanKey, GemmPlan>& plan_cache(const void* engine) {
   static std::map<const void*, std::map<PlanKey, GemmPlan>> caches;
-  return caches[engine];
+  auto& c = caches[engine];
+  // Plans are keyed by row count; a ragged corpus brings a new one nearly
+  // every batch. Graphs copy the tensor maps at capture, so dropping is safe.
+  if (c.size() >= 8192) c.clear();
+  return c;
 }
 
 Engine::Engine(HostModel model, int precision, int device)
@@ -293,7 +297,12 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
     cap_enc_ = m_enc;
   } else {
     cap_sent_ = std::max(n_sent, cap_sent_);
-    cap_enc_ = std::max(m_enc, cap_enc_);
+    // Encoder rows grow geometrically (up to every sentence at max_seq_len):
+    // a length-sorted corpus otherwise reallocates, re-plans and re-captures
+    // on almost every batch. Only buffer sizes depend on cap_enc_.
+    if (m_enc > cap_enc_)
+      cap_enc_ = std::max(
+          m_enc, std::min(2 * cap_enc_, cap_sent_ * std::max(host_.config.max_seq_len, 1)));
   }
   cap_beam_ = std::max(beam, cap_beam_);
   plan_cache(this).clear();
@@ -313,7 +322,6 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   enc_qkv_.resize(M * 3 * d);
   enc_ctx_.resize(M * d);
   ffh_.resize(size_t(act_rows_) * dff);
-  ckv_.clear();
   ckv_.resize(c.num_decoder_layers);
   for (auto& b : ckv_) b.resize(M * 2 * d);
   dec_y_.resize(r_max_ * d);
@@ -324,7 +332,6 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   part_m_.resize(size_t(r_max_) * part_ld_);
   part_s_.resize(size_t(r_max_) * part_ld_);
   part_arg_.resize(size_t(r_max_) * part_ld_);
-  qkv_cache_.clear();
   qkv_cache_.resize(c.num_decoder_layers);
   for (auto& b : qkv_cache_) b.resize(size_t(T_) * r_max_ * 3 * d);
   src_ids_.resize(M);
@@ -720,6 +727,14 @@ void Engine::run_encoder(int n_sent, int m, int max_src) {
     // shape (exact key: workspace generation, sizes, factor-id buffer).
     const EncKey key{ws_gen_, n_sent, m, max_src, src_fids_.get()};
     auto it = enc_graphs_.find(key);
+    // Capture a shape on its second use: a corpus of ragged batches (a new
+    // row count nearly every call) runs eagerly instead of paying a capture
+    // and instantiation per call.
+    if (it == enc_graphs_.end() && enc_seen_.insert(key).second) {
+      if (enc_seen_.size() >= 4096) enc_seen_.clear();
+      run_encoder_body(n_sent, m, max_src);
+      return;
+    }
     if (it == enc_graphs_.end()) {
       if (enc_graphs_.size() >= 256) clear_enc_graphs();
       const int64_t before = launches_;

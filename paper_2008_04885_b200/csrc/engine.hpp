@@ -7,6 +7,7 @@
 #include <memory>
 #include <mutex>
 #include <map>
+#include <set>
 #include <tuple>
 #include <string>
 #include <vector>
@@ -224,6 +225,7 @@ class Engine {
     }
   };
   std::map<EncKey, std::pair<cudaGraphExec_t, int64_t>> enc_graphs_;
+  std::set<EncKey> enc_seen_;
   void clear_enc_graphs();
   cudaGraph_t step_graph_ = nullptr;
   cudaGraphExec_t step_exec_ = nullptr;
