@@ -229,6 +229,10 @@ class Engine {
   void clear_enc_graphs();
   cudaGraph_t step_graph_ = nullptr;
   cudaGraphExec_t step_exec_ = nullptr;
+  cudaGraphExec_t multi_exec_ = nullptr;  // steps_per_graph() steps per launch
+  int steps_per_graph() const;
+  int64_t capture_steps(int k, cudaGraphExec_t* exec, cudaGraph_t* graph);
+  void capture_one_step();
   int64_t step_kernels_ = 0;
   int ws_gen_ = 0;
   struct StepKey {
