@@ -203,7 +203,8 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
     if (p.nst * stage < need) p.splits = 1;
   }
   p.smem = p.nst * stage + kGemmSmemExtra;
-  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
+  p.a_box = (p.m_tiles == 1 && !split_a) ? std::max(8, (m_max + 7) / 8 * 8) : 128;
+  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, p.a_box);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, bn);
   p.a2 = p.a;
   p.b2 = p.b;
@@ -213,7 +214,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   }
   if (a.prec == kPrecTF32x3) {
     if (!a.ptr_lo) fail(kStateError, "gemm: TF32x3 needs the activation lo part");
-    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 128);
+    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, p.a_box);
   }
   return p;
 }
@@ -250,11 +251,12 @@ GemmPlan plan_logits(const Operand& a, const Operand& b, int m_max, int n) {
   p.nst = std::min({kMaxStages, budget / stage, std::max(2, p.num_kb)});
   if (p.nst < 2) fail(kStateError, "logits: tile too large");
   p.smem = p.nst * stage + groups * kEpiStageBytes + kGemmSmemExtra;
-  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, 128);
+  p.a_box = p.m_tiles == 1 ? std::max(8, (m_max + 7) / 8 * 8) : 128;
+  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, p.a_box);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, p.bn);
   if (a.prec == kPrecTF32x3) {
     if (!a.ptr_lo || !b.ptr_lo) fail(kStateError, "logits: TF32x3 needs lo operands");
-    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 128);
+    p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, p.a_box);
     p.b2 = make_map(b.ptr_lo, b.prec, b.rows, b.k_pad, p.bn);
   } else {
     p.a2 = p.a;
@@ -263,7 +265,9 @@ GemmPlan plan_logits(const Operand& a, const Operand& b, int m_max, int n) {
   return p;
 }
 
-void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep_in, cudaStream_t stream) {
+  GemmEpilogue ep = ep_in;
+  ep.a_box = p.a_box;
   if (p.persistent) {
     if (!ep.part_m) fail(kStateError, "logits: softmax partial buffers missing");
     switch (p.prec) {

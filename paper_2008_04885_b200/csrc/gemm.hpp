@@ -36,6 +36,11 @@ struct GemmPlan {
   int smem = 0;    // dynamic shared memory bytes
   int splits = 1;  // split-K factor (grid.z)
   bool persistent = false;  // output projection: logits_tc_kernel
+  // Rows of the A tile fetched by TMA: m_max rounded up to 8 when one m tile
+  // covers all rows (decoding at small batch), else 128. The MMA still reads
+  // 128 rows; the rows beyond the box hold stale shared memory whose
+  // accumulator rows the epilogue masks and never stores.
+  int a_box = 128;
 };
 
 

@@ -33,6 +33,7 @@
 namespace mtg {
 
 struct GemmEpilogue {
+  int a_box;                 // A rows per TMA box (GemmPlan::a_box; set by launch_gemm)
   float* C;                  // output base
   long long ldc;             // row pitch of C (elements)
   long long c_step_stride;   // C += (*d_step) * c_step_stride when d_step != null
@@ -180,9 +181,9 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   // their first stages before the programmatic-dependency wait, so the weight
   // fetch overlaps the predecessor's tail. Everything that reads predecessor
   // outputs (A operand, row count, scales, residual) comes after pdl_wait.
-  constexpr int kABytes = kATile * (kSplit && !kSplitA ? 2 : 1);  // A bytes loaded by TMA
+  const int kABytes = ep.a_box * 128 * (kSplit && !kSplitA ? 2 : 1);  // A bytes loaded by TMA
   constexpr int kBBytes = kBTile * (kSplit ? 2 : 1);
-  constexpr int kLoadBytes = kABytes + kBBytes;
+  const int kLoadBytes = kABytes + kBBytes;
   const int npre = min(nst, kb_count);
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < npre; ++kb) {
@@ -418,6 +419,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         tmem_ld_wait();
       }
       if (n0 + c >= N) continue;  // warp-uniform
+      if (nrows < 32 && lane >= nrows) {  // rows past M: stale A rows (GemmPlan::a_box)
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) r[j] = 0u;
+      }
       float v[kChunk];
       if constexpr (PREC == kPrecI8) {
         if (ep.seg_width == 0 || ep.seg_width % kChunk == 0) {
@@ -547,7 +552,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         if (lane + o < 32 && os == sg) seg_max = fmaxf(seg_max, ov);
       }
       const int prev = __shfl_up_sync(0xffffffffu, sg, 1);
-      if (__any_sync(0xffffffffu, seg_bad) && lane == 0) atomicExch(ep.nonfinite, 1);
+      if (__any_sync(0xffffffffu, seg_bad && lane < nrows) && lane == 0)
+        atomicExch(ep.nonfinite, 1);
       if (sg >= 0 && (lane == 0 || prev != sg))
         atomicMax(ep.seg_absmax + sg, __float_as_uint(seg_max));
     }

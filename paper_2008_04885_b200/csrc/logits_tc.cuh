@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(64 + EG * 256, 1)
   const int m_live = (M + 127) / 128;
   const int total = m_live * n_tiles;
 
+  const int load_bytes = (ep.a_box * 128 + kBTile) * (kSplit ? 2 : 1);
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: one ring across all tiles ----
       int g = 0;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(64 + EG * 256, 1)
           const uint32_t ph = (g / nst) & 1;
           if (g >= nst) mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * kStageBytes;
-          mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+          mbar_arrive_expect_tx(&full_bar[s], load_bytes);
           tma_load_2d(st, &mapA, &full_bar[s], kb * kKbElems, m0);
           tma_load_2d(st + kATile, &mapB, &full_bar[s], kb * kKbElems, n0);
           if constexpr (kSplit) {
@@ -176,6 +177,10 @@ __global__ void __launch_bounds__(64 + EG * 256, 1)
         tmem_ld32(tmem + buf * kTmemCols + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
         if (nrows <= 0 || n0 + c >= N) continue;  // warp-uniform
+        if (nrows < 32 && lane >= nrows) {  // rows past M: stale A rows (GemmPlan::a_box)
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) r[j] = 0u;
+        }
         float v[kChunk];
 #pragma unroll
         for (int j = 0; j < kChunk; ++j)
