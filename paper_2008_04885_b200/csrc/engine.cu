@@ -573,11 +573,20 @@ void Engine::gemm_logits(int m, const int* d_m) {
     return e ? std::atoi(e) : -1;
   }();
   const bool persistent = persistent_env >= 0 ? persistent_env != 0 : prec_ == kF32;
+  // fp32: CTA-pair tiles (cta_group::2) cut the L2 -> SM operand traffic the
+  // TF32x3 projection is bound by (MTG_LOGITS_PAIR=0: one CTA per tile, A/B).
+  static const bool pair_env = [] {
+    const char* e = std::getenv("MTG_LOGITS_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  // One 128-row tile (small batches) gains nothing from a pair: single CTA.
+  const bool pair = persistent && pair_env && la.op().prec == kPrecTF32x3 && m > 128;
   if (it == cache.end())
     it = cache
-             .emplace(key, persistent ? plan_logits(la.op(), logits_w_.op(), m, logits_w_.n)
-                                      : plan_gemm(la.op(), logits_w_.op(), m, logits_w_.n, 0,
-                                                  128))
+             .emplace(key, pair         ? plan_logits_pair(la.op(), logits_w_.op(), m, logits_w_.n)
+                           : persistent ? plan_logits(la.op(), logits_w_.op(), m, logits_w_.n)
+                                        : plan_gemm(la.op(), logits_w_.op(), m, logits_w_.n, 0,
+                                                    128))
              .first;
   GemmEpilogue ep{};
   ep.C = logits_.get();

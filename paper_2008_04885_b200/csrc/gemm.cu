@@ -1,6 +1,7 @@
 // Host side of the tcgen05 GEMM: TMA tensor maps, tile-size choice, launch.
 #include "gemm.hpp"
 #include "logits_tc.cuh"
+#include "logits_tc2.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -265,9 +266,70 @@ GemmPlan plan_logits(const Operand& a, const Operand& b, int m_max, int n) {
   return p;
 }
 
+GemmPlan plan_logits_pair(const Operand& a, const Operand& b, int m_max, int n) {
+  if (a.prec != kPrecTF32x3 || b.prec != kPrecTF32x3 || a.k_pad != b.k_pad)
+    fail(kShapeError, "logits pair: TF32x3 operands with equal K");
+  if (!a.ptr_lo || !b.ptr_lo) fail(kStateError, "logits pair: TF32x3 needs lo operands");
+  GemmPlan p;
+  p.prec = a.prec;
+  p.persistent = true;
+  p.pair = true;
+  p.num_kb = a.k_pad * prec_elem_bytes(a.prec) / 128;
+  p.m_tiles = (m_max + 255) / 256;
+  p.bn = 256;
+  p.n_tiles = (n + p.bn - 1) / p.bn;
+  const int stage = 4 * 128 * 128;
+  const int budget = 227 * 1024 - kEpiStageBytes - kGemmSmemExtra;
+  p.nst = std::min({kMaxStages, budget / stage, std::max(2, p.num_kb)});
+  if (p.nst < 2) fail(kStateError, "logits pair: tile too large");
+  p.smem = p.nst * stage + kEpiStageBytes + kGemmSmemExtra;
+  p.a_box = m_max <= 128 ? std::max(8, (m_max + 7) / 8 * 8) : 128;
+  p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, p.a_box);
+  p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, p.a_box);
+  p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, 128);  // each CTA loads half the tile
+  p.b2 = make_map(b.ptr_lo, b.prec, b.rows, b.k_pad, 128);
+  return p;
+}
+
+static void launch_logits_pair(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    MTG_CUDA(cudaFuncSetAttribute(logits_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    configured = true;
+  }
+  if (!ep.part_m) fail(kStateError, "logits: softmax partial buffers missing");
+  if (ep.part_ld % 4 != 0 || ep.part_ld * 32 < ep.N)
+    fail(kStateError, "logits pair: softmax partial pitch");
+  // Tiles go round-robin to the pairs, m fastest (the pair tiles sharing a
+  // weight tile run together). With an even number of m tiles an odd pair
+  // count alternates each pair between the full first m tile and the
+  // partial last one instead of pinning half the pairs to the heavy tiles.
+  int pairs = std::min(74, p.m_tiles * p.n_tiles);
+  if (p.m_tiles % 2 == 0 && pairs % 2 == 0 && pairs > 1) --pairs;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  MTG_CUDA(cudaLaunchKernelEx(&cfg, logits_tc2_kernel, p.a, p.b, p.a2, p.b2, p.num_kb, p.nst,
+                              p.n_tiles, ep));
+  MTG_CUDA(cudaGetLastError());
+}
+
 void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep_in, cudaStream_t stream) {
   GemmEpilogue ep = ep_in;
   ep.a_box = p.a_box;
+  if (p.pair) return launch_logits_pair(p, ep, stream);
   if (p.persistent) {
     if (!ep.part_m) fail(kStateError, "logits: softmax partial buffers missing");
     switch (p.prec) {

@@ -36,6 +36,7 @@ struct GemmPlan {
   int smem = 0;    // dynamic shared memory bytes
   int splits = 1;  // split-K factor (grid.z)
   bool persistent = false;  // output projection: logits_tc_kernel
+  bool pair = false;        // ... as CTA pairs (logits_tc2_kernel, TF32x3)
   // Rows of the A tile fetched by TMA: m_max rounded up to 8 when one m tile
   // covers all rows (decoding at small batch), else 128. The MMA still reads
   // 128 rows; the rows beyond the box hold stale shared memory whose
@@ -53,6 +54,8 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n,
 // Output projection with softmax partials (logits_tc.cuh): persistent CTAs,
 // double-buffered TMEM accumulators. Launch with launch_gemm.
 GemmPlan plan_logits(const Operand& a, const Operand& b, int m_max, int n);
+// TF32x3 projection on CTA pairs (cta_group::2, 256 x 256 tiles; logits_tc2.cuh).
+GemmPlan plan_logits_pair(const Operand& a, const Operand& b, int m_max, int n);
 void launch_gemm(const GemmPlan& plan, const GemmEpilogue& ep, cudaStream_t stream);
 
 }  // namespace mtg

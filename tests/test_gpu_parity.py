@@ -337,6 +337,33 @@ def test_step_fusion_modes_agree():
     assert outs[0].strip() and all(o == outs[0] for o in outs)
 
 
+@pytest.mark.gpu
+def test_f32_projection_kernels_agree():
+    """The fp32 output projection runs on CTA pairs (cta_group::2, default),
+    one persistent CTA per tile (MTG_LOGITS_PAIR=0) or one tile per CTA
+    (MTG_LOGITS_PERSISTENT=0): same hypotheses and score bits. 60 sentences x
+    beam 5 = 300 rows covers a second, partly live pair tile."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2008_04885_b200 as mt, oracle_lib as o\n"
+        "from golden_util import f32hex\n"
+        "c = dict(num_encoder_layers=2, num_decoder_layers=2, d_model=64, d_ff=256, num_heads=4,"
+        " src_vocab_size=700, tgt_vocab_size=900, dropout=0.0, max_seq_len=64)\n"
+        "gm = mt.Model.create(c, seed=3, precision=mt.F32)\n"
+        "srcs = o.synthetic_sources(60, 9, 700, seed=2)\n"
+        "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs, mt.BeamConfig(5, 0, 1.0))])\n"
+        "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs[:1], mt.BeamConfig(5, 0, 1.0))])\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in (dict(), dict(MTG_LOGITS_PAIR="0"), dict(MTG_LOGITS_PERSISTENT="0")):
+        env = dict(os.environ, **v)
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
+                                   capture_output=True, text=True, timeout=300).stdout)
+    assert outs[0].strip() and all(o == outs[0] for o in outs)
+
+
 @pytest.mark.parametrize("combine,shared", [("concat", False), ("sum", False), ("average", True),
                                             ("sum", True)])
 def test_source_factors_bit_exact(combine, shared):
