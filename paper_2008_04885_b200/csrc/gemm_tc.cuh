@@ -312,7 +312,11 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     const int half = (warp - 2) >> 2;
     float* stage = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * 33);
     const int rbase = m0 + q * 32;
-    int nrows = min(32, M - rbase);  // warp-uniform, may be <= 0
+    // Split-K: the 8 (row quarter, column half) regions of the tile are
+    // reduced and stored by different splits of the cluster (region r by
+    // split r % splits), spreading the DSMEM reads over the SMs.
+    const bool owner = splits <= 1 || ((q * 2 + half) % splits) == z;
+    int nrows = owner ? min(32, M - rbase) : 0;  // warp-uniform, may be <= 0
     float inv[kMaxSegments];
     if constexpr (PREC == kPrecI8) {
       const float sa = lane < nrows ? ep.a_scale[rbase + lane] : 1.0f;
@@ -357,9 +361,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     mbar_wait(accum_bar, 0);
     tc_fence_after();
     // Split-K over a thread-block cluster along z: every split parks its raw
-    // accumulator tile in its own (drained) shared memory, then split 0 reads
-    // the others through DSMEM, sums them in z order (int32 exact, float
-    // ordered) and runs the epilogue. Two cluster barriers bracket the reads.
+    // accumulator tile in its own (drained) shared memory, then the owner of
+    // each region reads all splits' partials through DSMEM, sums them in z
+    // order (int32 exact, float ordered) and runs the epilogue for it. Two
+    // cluster barriers bracket the reads.
     constexpr int kPartPitch = BN + 4;  // words; conflict-free row-per-thread float4
     uint32_t* part = reinterpret_cast<uint32_t*>(smem + kEpiStageBytes);
     const uint32_t* my_part_row = part + (q * 32 + lane) * kPartPitch;
@@ -380,7 +385,6 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
               make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
       }
       cluster_sync_all();  // (1) all partials parked
-      if (z != 0) nrows = 0;  // only split 0 runs the epilogue
     }
 #pragma unroll 1
     for (int c = half * kHalf; c < (half + 1) * kHalf; c += kChunk) {
@@ -390,7 +394,9 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         const uint32_t my_addr = smem_u32(my_part_row + c);
 #pragma unroll
         for (int j = 0; j < kChunk; j += 4) {
-          uint4 a = *reinterpret_cast<const uint4*>(my_part_row + c + j);
+          // z order from split 0, whichever split owns the region
+          uint4 a = z == 0 ? *reinterpret_cast<const uint4*>(my_part_row + c + j)
+                           : dsmem_ld4(dsmem_map(my_addr + 4 * j, 0));
           for (int zz = 1; zz < splits; ++zz) {
             const uint4 b = dsmem_ld4(dsmem_map(my_addr + 4 * j, zz));
             if constexpr (PREC == kPrecI8) {
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         }
       }
     }
-    if (splits > 1) cluster_sync_all();  // (2) split 0 is done reading the partials
+    if (splits > 1) cluster_sync_all();  // (2) every owner is done reading the partials
   }
 
   tc_fence_before();
