@@ -171,14 +171,13 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   // >= ~160 KB of operand bytes per split, at most 8 (portable cluster).
   // MTG_SPLIT_CTAS / MTG_SPLIT_KB override the target grid size and bytes
   // per split (A/B experiments); default 160 KB per split.
-  // Single-m-tile GEMMs (batch-1 decoding) are pure latency: aim for two
-  // CTAs per SM there (measured: fp32 p90 batch-1 -9 %); one per SM otherwise
-  // (batch-64 throughput drops with more splits).
+  // Aim for two CTAs per SM (measured: fp32 p90 batch-1 -9 %, and with the
+  // distributed split-K epilogue fp32 batch-64 +0.5 % over one per SM).
   static const int split_ctas_env = [] {
     const char* e = std::getenv("MTG_SPLIT_CTAS");
     return e ? std::atoi(e) : 0;
   }();
-  const int split_ctas = split_ctas_env > 0 ? split_ctas_env : (p.m_tiles == 1 ? 296 : 148);
+  const int split_ctas = split_ctas_env > 0 ? split_ctas_env : 296;
   static const long long split_bytes = [] {
     const char* e = std::getenv("MTG_SPLIT_KB");
     return (e ? std::atoll(e) : 160LL) * 1024;
