@@ -159,6 +159,16 @@ Operand ActOperand::op() const {
 // construction / weights
 // ============================================================================
 
+// Narrowest GEMM tile the planner may pick (MTG_MIN_BN A/B switch; default 32).
+static int gemm_min_bn() {
+  static const int v = [] {
+    const char* e = std::getenv("MTG_MIN_BN");
+    const int b = e ? std::atoi(e) : 32;
+    return (b == 64 || b == 128) ? b : 32;
+  }();
+  return v;
+}
+
 static std::map<PlanKey, GemmPlan>& plan_cache(const void* engine) {
   static std::map<const void*, std::map<PlanKey, GemmPlan>> caches;
   auto& c = caches[engine];
@@ -448,7 +458,7 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
   if (it == cache.end())
-    it = cache.emplace(key, plan_gemm(a.op(), w.op(), m, w.n, 0, 32, split_k_)).first;
+    it = cache.emplace(key, plan_gemm(a.op(), w.op(), m, w.n, 0, gemm_min_bn(), split_k_)).first;
   GemmEpilogue ep{};
   ep.C = c;
   ep.ldc = ldc;
