@@ -169,6 +169,24 @@ static int gemm_min_bn() {
   return v;
 }
 
+// Tile width forced for large-M (encoder) GEMMs (MTG_ENC_BN A/B switch; 0 = planner).
+// MTG_ENC_BN_MAP="NxK:bn,..." overrides per shape (tuning).
+static int enc_force_bn(int n, int k) {
+  static const std::string map = [] {
+    const char* e = std::getenv("MTG_ENC_BN_MAP");
+    return std::string(e ? e : "");
+  }();
+  const std::string key = std::to_string(n) + "x" + std::to_string(k) + ":";
+  const auto pos = map.find(key);
+  if (pos != std::string::npos) return std::atoi(map.c_str() + pos + key.size());
+  static const int v = [] {
+    const char* e = std::getenv("MTG_ENC_BN");
+    const int b = e ? std::atoi(e) : 0;
+    return (b == 32 || b == 64 || b == 128 || b == 256) ? b : 0;
+  }();
+  return v;
+}
+
 static std::map<PlanKey, GemmPlan>& plan_cache(const void* engine) {
   static std::map<const void*, std::map<PlanKey, GemmPlan>> caches;
   auto& c = caches[engine];
@@ -458,7 +476,11 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
   if (it == cache.end())
-    it = cache.emplace(key, plan_gemm(a.op(), w.op(), m, w.n, 0, gemm_min_bn(), split_k_)).first;
+    it = cache
+             .emplace(key, plan_gemm(a.op(), w.op(), m, w.n,
+                                     m > 512 ? enc_force_bn(w.n, a.op().k_pad) : 0,
+                                     gemm_min_bn(), split_k_))
+             .first;
   GemmEpilogue ep{};
   ep.C = c;
   ep.ldc = ldc;
