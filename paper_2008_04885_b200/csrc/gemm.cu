@@ -142,6 +142,13 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
 
 }  // namespace
 
+// Fewest m tiles for the long-K 64-column rule below (MTG_LONGK_MTILES A/B;
+// measured: 3 -> decoder FFN-down at batch 64 f32 +3.1 %; 1 -> batch-1 p90 +4 %).
+static const int kLongKMinMTiles = [] {
+  const char* e = std::getenv("MTG_LONGK_MTILES");
+  return e ? std::atoi(e) : 3;
+}();
+
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn,
                    int min_bn, bool allow_split) {
   const bool split_a = a.prec == kPrecTF32x3A && b.prec == kPrecTF32x3;  // plain fp32 A
@@ -162,10 +169,10 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
         break;
       }
     }
-    // Many m tiles and a long fp32 K stream (the encoder's FFN-down): 32-column
-    // tiles re-read the hi+lo A rows once per tile; 64 columns with a split-K
-    // of 2 measured faster (fp32 encoder -6 %, batch +1.3 %; bf16 -0.2 %).
-    if (bn == 32 && p.m_tiles >= 4 && prec_is_tf32x3(b.prec) &&
+    // Several m tiles and a long fp32 K stream (the FFN-down GEMMs): 32-column
+    // tiles re-read the hi+lo A rows once per tile; 64 columns with split-K
+    // measured faster (fp32 encoder -6 %, decoder +3 % at batch 64; bf16 -0.2 %).
+    if (bn == 32 && p.m_tiles >= kLongKMinMTiles && prec_is_tf32x3(b.prec) &&
         a.k_pad * prec_elem_bytes(a.prec) / 128 >= 32)
       bn = 64;
     bn = std::max(bn, min_bn);
