@@ -149,6 +149,12 @@ static const int kLongKMinMTiles = [] {
   return e ? std::atoi(e) : 3;
 }();
 
+static const int kLongKBn = [] {
+  const char* e = std::getenv("MTG_LONGK_BN");
+  const int v = e ? std::atoi(e) : 64;
+  return (v == 128 || v == 256) ? v : 64;
+}();
+
 GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int force_bn,
                    int min_bn, bool allow_split) {
   const bool split_a = a.prec == kPrecTF32x3A && b.prec == kPrecTF32x3;  // plain fp32 A
@@ -174,7 +180,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
     // measured faster (fp32 encoder -6 %, decoder +3 % at batch 64; bf16 -0.2 %).
     if (bn == 32 && p.m_tiles >= kLongKMinMTiles && prec_is_tf32x3(b.prec) &&
         a.k_pad * prec_elem_bytes(a.prec) / 128 >= 32)
-      bn = 64;
+      bn = kLongKBn;
     bn = std::max(bn, min_bn);
   }
   p.bn = bn;
