@@ -122,6 +122,7 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
   // +1.5 % int8; the same for the encoder's BN = 128 GEMMs was neutral).
   const int fl = (ep.bias ? 1 : 0) | (ep.relu ? 2 : 0) | (ep.residual ? 4 : 0) |
                  (ep.d_step ? 8 : 0);
+  if (p.bn == 64 && fl == 5) return launch_one<PREC, 64, kEpiLinear, 5>(p, ep, stream);  // FFN-down
   if (p.bn == 32) {
     switch (fl) {
       case 0: return launch_one<PREC, 32, kEpiLinear, 0>(p, ep, stream);
