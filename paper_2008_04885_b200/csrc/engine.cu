@@ -233,6 +233,7 @@ Engine::~Engine() {
   if (multi_exec_) cudaGraphExecDestroy(multi_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);
   if (h_pinned_) cudaFreeHost(h_pinned_);
+  if (res_host_) cudaFreeHost(res_host_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -1158,18 +1159,35 @@ std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vecto
   const int n = staged_n_;
   std::vector<SentenceResult> out(n);
   if (n == 0) return out;
-  std::vector<int> len(n), status(n), tok(size_t(n) * T_);
-  std::vector<float> lp(n), norm(n);
-  std::vector<unsigned> flags(n);
+  // All results in one pinned staging area: the copies queue behind the
+  // decode loop and the host waits once.
+  const size_t nt = size_t(n) * T_;
+  const size_t words = 5 * size_t(n) + nt + 1;
+  if (words > res_host_words_) {
+    if (res_host_) cudaFreeHost(res_host_);
+    res_host_ = nullptr;
+    MTG_CUDA(cudaMallocHost(&res_host_, words * sizeof(int)));
+    res_host_words_ = words;
+  }
+  int* const len = res_host_;
+  int* const status = len + n;
+  float* const lp = reinterpret_cast<float*>(status + n);
+  float* const norm = lp + n;
+  unsigned* const flags = reinterpret_cast<unsigned*>(norm + n);
+  int* const tok = reinterpret_cast<int*>(flags + n);
+  int* const badp = tok + nt;
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    MTG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_));
+  };
+  d2h(len, res_len_.get(), n * sizeof(int));
+  d2h(status, res_status_.get(), n * sizeof(int));
+  d2h(lp, res_lp_.get(), n * sizeof(float));
+  d2h(norm, res_norm_.get(), n * sizeof(float));
+  d2h(flags, res_flags_.get(), n * sizeof(unsigned));
+  d2h(tok, res_tok_.get(), nt * sizeof(int));
+  d2h(badp, nonfinite_.get(), sizeof(int));
   MTG_CUDA(cudaStreamSynchronize(stream_));
-  res_len_.download(len.data(), n, stream_);
-  res_status_.download(status.data(), n, stream_);
-  res_lp_.download(lp.data(), n, stream_);
-  res_norm_.download(norm.data(), n, stream_);
-  res_flags_.download(flags.data(), n, stream_);
-  res_tok_.download(tok.data(), tok.size(), stream_);
-  int bad = 0;
-  nonfinite_.download(&bad, 1, stream_);
+  const int bad = *badp;
   for (int s = 0; s < n; ++s) {
     SentenceResult& r = out[s];
     if (staged_status_[s]) {
@@ -1180,7 +1198,7 @@ std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vecto
     r.status = bad ? kValueError : status[s];
     r.flags = bad ? 4u : flags[s];
     if (r.status) continue;
-    r.tokens.assign(tok.begin() + size_t(s) * T_, tok.begin() + size_t(s) * T_ + len[s]);
+    r.tokens.assign(tok + size_t(s) * T_, tok + size_t(s) * T_ + len[s]);
     r.logprob = lp[s];
     r.norm = norm[s];
   }

@@ -206,6 +206,8 @@ class Engine {
   DeviceBuffer<unsigned> res_flags_;
   BeamDev beam_{};
   int* h_pinned_ = nullptr;  // pinned host mailbox (n_rows polling)
+  int* res_host_ = nullptr;  // pinned staging of a batch's results
+  size_t res_host_words_ = 0;
 
   // staged batch (benchmark)
   std::vector<std::vector<int>> staged_;
