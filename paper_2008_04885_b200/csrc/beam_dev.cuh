@@ -210,14 +210,18 @@ __device__ __forceinline__ void finish_select(const BeamDev& b, int t, int* live
                                               int* is_last) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Last-CTA election: every CTA's writes are made visible before its ticket.
+  // A single-CTA grid (batch-1) is its own last CTA: the block barrier makes
+  // its global writes visible to its threads without the fence round trips.
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (gridDim.x > 1) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      *is_last = atomicAdd(b.sel_count, 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!*is_last) return;
     __threadfence();
-    *is_last = atomicAdd(b.sel_count, 1) == static_cast<int>(gridDim.x) - 1;
   }
-  __syncthreads();
-  if (!*is_last) return;
-  __threadfence();
   for (int s = threadIdx.x; s < b.N; s += blockDim.x) live_s[s] = __ldcg(b.sent_live + s);
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the live counts (32 sentences per pass)
