@@ -85,6 +85,19 @@ __global__ void beam_reorder_kernel(BeamDev b) {
 
 }  // namespace
 
+// While-node condition of the device-side decode loop: another chunk of k
+// steps while hypotheses are alive and the chunk fits below loop_end.
+__global__ void decode_loop_cond_kernel(cudaGraphConditionalHandle h, const int* n_rows,
+                                        const int* step, const int* loop_end, int k) {
+  cudaGraphSetConditional(h, (*n_rows > 0 && *step + k <= *loop_end) ? 1u : 0u);
+}
+
+void launch_decode_loop_cond(cudaGraphConditionalHandle h, const int* n_rows, const int* step,
+                             const int* loop_end, int k, cudaStream_t st) {
+  decode_loop_cond_kernel<<<1, 1, 0, st>>>(h, n_rows, step, loop_end, k);
+  MTG_CUDA(cudaGetLastError());
+}
+
 void launch_beam_init(const BeamDev& b, cudaStream_t st) {
   launch_k(beam_init_kernel, 1, 32, 0, st, b);
   MTG_CUDA(cudaGetLastError());

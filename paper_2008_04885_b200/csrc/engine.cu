@@ -231,6 +231,7 @@ Engine::~Engine() {
   plan_cache(this).clear();
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (multi_exec_) cudaGraphExecDestroy(multi_exec_);
+  if (loop_exec_) cudaGraphExecDestroy(loop_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);
   if (h_pinned_) cudaFreeHost(h_pinned_);
   if (res_host_) cudaFreeHost(res_host_);
@@ -1033,17 +1034,67 @@ void Engine::ensure_step_graph() {
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);
   if (multi_exec_) cudaGraphExecDestroy(multi_exec_);
+  if (loop_exec_) cudaGraphExecDestroy(loop_exec_);
   step_exec_ = nullptr;
   step_graph_ = nullptr;
   multi_exec_ = nullptr;
+  loop_exec_ = nullptr;
   diag_clear();
   step_kernels_ = capture_steps(1, &step_exec_, &step_graph_);
   if (steps_per_graph() > 1 && !diag_) {
     cudaGraph_t g = nullptr;
     capture_steps(steps_per_graph(), &multi_exec_, &g);
     cudaGraphDestroy(g);
+    static const bool device_loop = [] {
+      const char* e = std::getenv("MTG_DEVICE_LOOP");
+      return !(e && e[0] == '0');
+    }();
+    if (device_loop) capture_device_loop(steps_per_graph());
   }
   step_key_ = key;
+}
+
+// The decode loop as one graph: a while node whose body is k steps plus a
+// condition kernel (hypotheses alive and another k steps below loop_end),
+// so the host neither polls nor relaunches between chunks.
+void Engine::capture_device_loop(int k) {
+  loop_end_.resize(1);
+  cudaGraph_t g = nullptr;
+  MTG_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  MTG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  MTG_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const int64_t before = launches_;
+  MTG_CUDA(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+  capturing_ = true;
+  try {
+    for (int rep = 0; rep < k; ++rep) capture_one_step();
+    launch_decode_loop_cond(h, n_rows_.get(), step_.get(), loop_end_.get(), k, stream_);
+  } catch (...) {
+    capturing_ = false;
+    cudaGraph_t tmp = nullptr;
+    cudaStreamEndCapture(stream_, &tmp);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  capturing_ = false;
+  cudaGraph_t captured = nullptr;
+  MTG_CUDA(cudaStreamEndCapture(stream_, &captured));
+  const cudaError_t err = cudaGraphInstantiate(&loop_exec_, g, 0);
+  cudaGraphDestroy(g);
+  launches_ = before;
+  if (err != cudaSuccess) {  // fall back to host-driven chunks
+    cudaGetLastError();
+    loop_exec_ = nullptr;
+  }
 }
 
 int Engine::steps_per_graph() const {
@@ -1118,7 +1169,22 @@ void Engine::decode_loop(int t_run) {
   count();
   ensure_step_graph();
   const int k = multi_exec_ ? steps_per_graph() : 1;
-  for (int t = 0; t < t_run; ++t) {
+  int t0 = 0;
+  if (loop_exec_ && t_run >= k) {
+    // Device loop over the whole k-step chunks (stops early once every
+    // hypothesis is done), then the remaining steps; steps after completion
+    // are no-ops (no live rows).
+    const int t_loop = t_run / k * k;
+    loop_end_.upload(&t_loop, 1, stream_);
+    MTG_CUDA(cudaGraphLaunch(loop_exec_, stream_));
+    launches_ += static_cast<int64_t>(t_loop) * step_kernels_ + t_loop / k;  // + conditions
+    for (int t = t_loop; t < t_run; ++t) {
+      MTG_CUDA(cudaGraphLaunch(step_exec_, stream_));
+      launches_ += step_kernels_;
+    }
+    return;
+  }
+  for (int t = t0; t < t_run; ++t) {
     if (k > 1 && t % k == 0 && t + k <= t_run) {
       MTG_CUDA(cudaGraphLaunch(multi_exec_, stream_));
       launches_ += k * step_kernels_;

@@ -232,6 +232,9 @@ class Engine {
   cudaGraph_t step_graph_ = nullptr;
   cudaGraphExec_t step_exec_ = nullptr;
   cudaGraphExec_t multi_exec_ = nullptr;  // steps_per_graph() steps per launch
+  cudaGraphExec_t loop_exec_ = nullptr;   // while node over multi-step bodies
+  DeviceBuffer<int> loop_end_;
+  void capture_device_loop(int k);
   int steps_per_graph() const;
   int64_t capture_steps(int k, cudaGraphExec_t* exec, cudaGraph_t* graph);
   void capture_one_step();

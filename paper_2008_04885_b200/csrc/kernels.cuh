@@ -167,6 +167,8 @@ struct BeamDev {
 
 // Step 0: one root row (BOS, logprob 0) per active sentence.
 void launch_beam_init(const BeamDev& b, cudaStream_t st);
+void launch_decode_loop_cond(cudaGraphConditionalHandle h, const int* n_rows, const int* step,
+                             const int* loop_end, int k, cudaStream_t st);
 
 // log_softmax_row + candidate scores + per-row top-min(B,V) by (score desc,
 // token asc), one warp per live row, from the per-32-column softmax partials
