@@ -10,6 +10,9 @@ python bench.py --impl reference --steps 2 --warmup 1 --precision f32 > gpurun_o
 cat gpurun_out/bench_*.json
 python tools/diag_step.py f32 > gpurun_out/diag_f32.txt 2>&1
 python tools/diag_step.py int8 > gpurun_out/diag_int8.txt 2>&1
+# ncu cannot profile kernels inside graphs with conditional (while) nodes:
+# the profiled runs drive the same step graphs from the host (MTG_DEVICE_LOOP=0).
+export MTG_DEVICE_LOOP=0
 for p in int8 f32; do
 python tools/profile_step.py $p > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_$p.csv python tools/profile_step.py $p > /dev/null 2>&1
 done
