@@ -594,6 +594,16 @@ ShortlistArgs Engine::shortlist_args() const {
   return a;
 }
 
+// Tile width of the one-tile-per-CTA projection (MTG_LOGITS_BN A/B; 0 = planner).
+static int logits_force_bn() {
+  static const int v = [] {
+    const char* e = std::getenv("MTG_LOGITS_BN");
+    const int b = e ? std::atoi(e) : 0;
+    return (b == 128 || b == 256) ? b : 0;
+  }();
+  return v;
+}
+
 void Engine::gemm_logits(int m, const int* d_m) {
   auto& cache = plan_cache(this);
   ActOperand& la = logits_act();
@@ -619,8 +629,8 @@ void Engine::gemm_logits(int m, const int* d_m) {
     it = cache
              .emplace(key, pair         ? plan_logits_pair(la.op(), logits_w_.op(), m, logits_w_.n)
                            : persistent ? plan_logits(la.op(), logits_w_.op(), m, logits_w_.n)
-                                        : plan_gemm(la.op(), logits_w_.op(), m, logits_w_.n, 0,
-                                                    128))
+                                        : plan_gemm(la.op(), logits_w_.op(), m, logits_w_.n,
+                                                    logits_force_bn(), 128))
              .first;
   GemmEpilogue ep{};
   ep.C = logits_.get();
@@ -1145,7 +1155,11 @@ void Engine::capture_one_step() {
     }();
     const int sl_prec = prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2;
     const ShortlistArgs sla = shortlist_args();
-    if (fused_tail && beam_.N >= 8) {  // measured: neutral-to-worse for batch-1
+    static const int fused_min_n = [] {  // measured: neutral-to-worse for batch-1
+      const char* e = std::getenv("MTG_FUSED_TAIL_MIN_N");
+      return e ? std::atoi(e) : 8;
+    }();
+    if (fused_tail && beam_.N >= fused_min_n) {
       launch_topk_select(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
                          part_ld_, use_shortlist_ ? &sla : nullptr, sl_prec, beam_, stream_);
       count("top-k + beam select");
