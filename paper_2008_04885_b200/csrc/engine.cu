@@ -187,6 +187,17 @@ static int enc_force_bn(int n, int k) {
   return v;
 }
 
+// MTG_DEC_BN_MAP="NxK:bn,..." forces tile widths of the small-M (decoder) GEMMs (tuning).
+static int dec_force_bn(int n, int k) {
+  static const std::string map = [] {
+    const char* e = std::getenv("MTG_DEC_BN_MAP");
+    return std::string(e ? e : "");
+  }();
+  const std::string key = std::to_string(n) + "x" + std::to_string(k) + ":";
+  const auto pos = map.find(key);
+  return pos == std::string::npos ? 0 : std::atoi(map.c_str() + pos + key.size());
+}
+
 static std::map<PlanKey, GemmPlan>& plan_cache(const void* engine) {
   static std::map<const void*, std::map<PlanKey, GemmPlan>> caches;
   auto& c = caches[engine];
@@ -480,7 +491,8 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   if (it == cache.end())
     it = cache
              .emplace(key, plan_gemm(a.op(), w.op(), m, w.n,
-                                     m > 512 ? enc_force_bn(w.n, a.op().k_pad) : 0,
+                                     m > 512 ? enc_force_bn(w.n, a.op().k_pad)
+                                             : dec_force_bn(w.n, a.op().k_pad),
                                      gemm_min_bn(), split_k_))
              .first;
   GemmEpilogue ep{};
