@@ -343,7 +343,9 @@ def test_f32_projection_kernels_agree():
     """The fp32 output projection runs on CTA pairs (cta_group::2, default),
     one persistent CTA per tile (MTG_LOGITS_PAIR=0) or one tile per CTA
     (MTG_LOGITS_PERSISTENT=0): same hypotheses and score bits. 60 sentences x
-    beam 5 = 300 rows covers a second, partly live pair tile."""
+    beam 5 = 300 rows covers a second, partly live pair tile; 30 sentences
+    (150 rows) one pair tile whose second CTA is partly live; 1 sentence the
+    single-CTA kernel."""
     import subprocess
     import sys
     code = (
@@ -356,6 +358,7 @@ def test_f32_projection_kernels_agree():
         "srcs = o.synthetic_sources(60, 9, 700, seed=2)\n"
         "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs, mt.BeamConfig(5, 0, 1.0))])\n"
         "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs[:1], mt.BeamConfig(5, 0, 1.0))])\n"
+        "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs[:30], mt.BeamConfig(5, 0, 1.0))])\n"
     ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for v in (dict(), dict(MTG_LOGITS_PAIR="0"), dict(MTG_LOGITS_PERSISTENT="0")):
