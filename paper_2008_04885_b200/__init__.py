@@ -23,6 +23,7 @@ Errors map onto the reference exception taxonomy (errors.hpp:8-34).
 from __future__ import annotations
 
 import ctypes
+import itertools
 import dataclasses
 import json
 import os
@@ -259,11 +260,11 @@ def _factor_block(factors, off, n_factors: int):
 
 def _csr(sources: Sequence[Sequence[int]]):
     off = np.zeros(len(sources) + 1, np.int64)
-    for i, s in enumerate(sources):
-        off[i + 1] = off[i] + len(s)
-    ids = np.zeros(max(int(off[-1]), 1), np.int32)
-    for i, s in enumerate(sources):
-        ids[off[i]:off[i + 1]] = np.asarray(s, np.int32)
+    np.cumsum([len(s) for s in sources], out=off[1:])
+    total = int(off[-1])
+    ids = np.zeros(max(total, 1), np.int32)
+    if total:
+        ids[:total] = np.fromiter(itertools.chain.from_iterable(sources), np.int64, total)
     return ids, off
 
 
