@@ -66,6 +66,17 @@ def test_beam_search_validates_before_touching_the_device():  # decode.cpp:38-39
         mt.beam_search(None, [], config=mt.BeamConfig(beam_size=1))
 
 
+def test_csr_packing():
+    """Sources reach the C ABI as CSR (ids int32, offsets int64)."""
+    ids, off = mt._csr([[5, 6, 3], [3], [7, 8, 9, 3]])
+    assert ids.dtype == np.int32 and off.dtype == np.int64
+    assert ids.tolist() == [5, 6, 3, 3, 7, 8, 9, 3] and off.tolist() == [0, 3, 4, 8]
+    ids, off = mt._csr([])
+    assert off.tolist() == [0] and ids.size == 1  # never a zero-length buffer
+    ids, off = mt._csr([[], [4, 3]])
+    assert off.tolist() == [0, 0, 2] and ids[:2].tolist() == [4, 3]
+
+
 def test_partition_balances_and_covers():
     rng = np.random.default_rng(1)
     lengths = rng.integers(5, 61, 1000).tolist()
