@@ -307,6 +307,8 @@ GemmPlan plan_logits_pair(const Operand& a, const Operand& b, int m_max, int n) 
   p.a2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, p.a_box);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, 128);  // each CTA loads half the tile
   p.b2 = make_map(b.ptr_lo, b.prec, b.rows, b.k_pad, 128);
+  p.at = make_map(a.ptr, a.prec, a.rows, a.k_pad, 64);    // M = 128 pair tiles
+  p.at2 = make_map(a.ptr_lo, a.prec, a.rows, a.k_pad, 64);
   return p;
 }
 
@@ -340,8 +342,8 @@ static void launch_logits_pair(const GemmPlan& p, const GemmEpilogue& ep, cudaSt
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  MTG_CUDA(cudaLaunchKernelEx(&cfg, logits_tc2_kernel, p.a, p.b, p.a2, p.b2, p.num_kb, p.nst,
-                              p.n_tiles, ep));
+  MTG_CUDA(cudaLaunchKernelEx(&cfg, logits_tc2_kernel, p.a, p.b, p.a2, p.b2, p.at, p.at2,
+                              p.num_kb, p.nst, p.n_tiles, ep));
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -27,6 +27,7 @@ struct Operand {
 
 struct GemmPlan {
   CUtensorMap a, b, a2, b2;
+  CUtensorMap at, at2;  // CTA-pair projection: 64-row A boxes (M = 128 pair tiles)
   int prec = 0;
   int bn = 0;
   int num_kb = 0;

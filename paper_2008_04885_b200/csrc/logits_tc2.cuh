@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(320, 1)
     logits_tc2_kernel(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB,
                       const __grid_constant__ CUtensorMap mapA2,
-                      const __grid_constant__ CUtensorMap mapB2, int num_kb, int nst, int n_tiles,
-                      GemmEpilogue ep) {
+                      const __grid_constant__ CUtensorMap mapB2,
+                      const __grid_constant__ CUtensorMap mapA64,
+                      const __grid_constant__ CUtensorMap mapA2_64, int num_kb, int nst,
+                      int n_tiles, GemmEpilogue ep) {
   constexpr int BN = 256;             // pair tile width (each CTA loads 128 B rows)
   constexpr int kKind = prec_mma_kind(kPrecTF32x3);
   constexpr int kKbElems = 32;        // fp32 elements per 128-byte slab
@@ -146,6 +148,8 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch_desc(&mapB);
       tma_prefetch_desc(&mapA2);
       tma_prefetch_desc(&mapB2);
+      tma_prefetch_desc(&mapA64);
+      tma_prefetch_desc(&mapA2_64);
     }
     pair2::tmem_alloc2<2 * kTmemCols>(tmem_slot);
   } else if (warp == 1 && lane == 0) {
@@ -178,21 +182,27 @@ __global__ void __launch_bounds__(320, 1)
       int g = 0;
       for (int t = pair; t < total; t += npairs) {
         const int mp = (t % m_pairs) * 256, n0 = (t / m_pairs) * BN;
-        const int my_m0 = mp + 128 * static_cast<int>(rank);
+        // A last pair tile of <= 128 live rows runs as an M = 128 pair MMA
+        // (64 rows per CTA): half the MMA time of M = 256.
+        const bool light = M - mp <= 128;
+        const int arows = light ? 64 : 128;
+        const int my_m0 = mp + arows * static_cast<int>(rank);
         const bool a_mine = my_m0 < M;
-        const bool a_peer = mp + 128 < M;  // the leader's A rows are always live
+        const bool a_peer = mp + arows < M;  // the leader's A rows are always live
+        const int a_bytes_t = light ? 64 * 128 : a_bytes;
         for (int kb = 0; kb < num_kb; ++kb, ++g) {
           const int s = g % nst;
           const uint32_t ph = (g / nst) & 1;
           if (g >= nst) pair2::wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * kStageBytes;
           if (leader)  // A hi+lo of each live half, B hi+lo of both halves
-            mbar_arrive_expect_tx(&full_bar[s], 2 * (a_bytes * (a_peer ? 2 : 1) + 2 * kHalfTile));
+            mbar_arrive_expect_tx(&full_bar[s], 2 * (a_bytes_t * (a_peer ? 2 : 1) + 2 * kHalfTile));
           const uint32_t fb = full0 + s * 8;
           const int kx = kb * kKbElems;
           if (a_mine) {
-            pair2::tma_load_2d_pair(st, &mapA, fb, kx, my_m0);
-            pair2::tma_load_2d_pair(st + 2 * kHalfTile, &mapA2, fb, kx, my_m0);
+            pair2::tma_load_2d_pair(st, light ? &mapA64 : &mapA, fb, kx, my_m0);
+            pair2::tma_load_2d_pair(st + 2 * kHalfTile, light ? &mapA2_64 : &mapA2, fb, kx,
+                                    my_m0);
           }
           pair2::tma_load_2d_pair(st + kHalfTile, &mapB, fb, kx, n0 + 128 * static_cast<int>(rank));
           pair2::tma_load_2d_pair(st + 3 * kHalfTile, &mapB2, fb, kx,
@@ -202,10 +212,12 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---- MMA issuer (leader only) ----
-      constexpr uint32_t idesc = make_idesc(kKind, 256, BN);
+      constexpr uint32_t idesc256 = make_idesc(kKind, 256, BN);
+      constexpr uint32_t idesc128 = make_idesc(kKind, 128, BN);
       int g = 0, i = 0;
       for (int t = pair; t < total; t += npairs, ++i) {
         const int buf = i & 1;
+        const uint32_t idesc = (M - (t % m_pairs) * 256 <= 128) ? idesc128 : idesc256;
         if (i >= 2) pair2::wait(&tempty_bar[buf], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + buf * kTmemCols;
@@ -244,9 +256,17 @@ __global__ void __launch_bounds__(320, 1)
     int i = 0;
     for (int t = pair; t < total; t += npairs, ++i) {
       const int buf = i & 1;
-      const int m0 = (t % m_pairs) * 256 + 128 * static_cast<int>(rank);
+      const int mp = (t % m_pairs) * 256;
       const int n0 = (t / m_pairs) * BN;
-      const int rbase = m0 + q * 32;
+      // M = 256 tiles: lanes = this CTA's 128 rows, TMEM columns = the 256
+      // output columns. M = 128 tiles (64 rows per CTA): lanes 0-63 hold
+      // columns 0-127 and lanes 64-127 columns 128-255 of the same 64 rows.
+      const bool light = M - mp <= 128;
+      const int rbase = light ? mp + 64 * static_cast<int>(rank) + (q & 1) * 32
+                              : mp + 128 * static_cast<int>(rank) + q * 32;
+      const int cb = light ? (q >> 1) * 128 : 0;        // output column of TMEM column 0
+      const int c_lo = light ? half * 64 : half * kHalf;  // this warp's TMEM columns
+      const int c_hi = c_lo + (light ? 64 : kHalf);
       const int nrows = min(32, M - rbase);  // warp-uniform, may be <= 0
       float* const Cbase = ep.C + static_cast<long long>(rbase) * ldc;
       float sub_m[kSubs], sub_s[kSubs];
@@ -254,11 +274,11 @@ __global__ void __launch_bounds__(320, 1)
       pair2::wait(&tfull_bar[buf], (i >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * kHalf; c < (half + 1) * kHalf; c += kChunk) {
+      for (int c = c_lo; c < c_hi; c += kChunk) {
         uint32_t r[32];
         tmem_ld32(tmem + buf * kTmemCols + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
-        if (nrows <= 0 || n0 + c >= N) continue;  // warp-uniform
+        if (nrows <= 0 || n0 + cb + c >= N) continue;  // warp-uniform
         if (nrows < 32 && lane >= nrows) {  // rows past M: stale or zero A rows
 #pragma unroll
           for (int j = 0; j < kChunk; ++j) r[j] = 0u;
@@ -269,7 +289,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) stage[lane * 33 + j] = v[j];
         // Slice max / first argmax (strict >), sequential sum of exp(x - max).
-        const int col0 = n0 + c;
+        const int col0 = n0 + cb + c;
         const int nv = min(kChunk, N - col0);
         float best = -__int_as_float(0x7f800000);
         float mn = __int_as_float(0x7f800000);
@@ -283,7 +303,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         const float sum =
             det_sum_exp(stage + lane * 33, bi >= 0 ? nv : 0, best, bi >= 0 ? mn : 0.0f);
-        const int k = (c - half * kHalf) / 32;
+        const int k = (c - c_lo) / 32;
 #pragma unroll
         for (int kk = 0; kk < kSubs; ++kk)
           if (kk == k) {
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(320, 1)
             sub_a[kk] = bi;
           }
         __syncwarp();
-        const int col = n0 + c + lane;
+        const int col = col0 + lane;
         if (col < N) {
           float* cp = Cbase + col;
 #pragma unroll 8
@@ -305,11 +325,20 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) pair2::arrive_remote(tempty0 + buf * 8);
-      const int sub0 = (n0 + half * kHalf) / 32;
+      const int sub0 = (n0 + cb + c_lo) / 32;
       const int nsub = (N + 31) / 32;
+      const int my_subs = (c_hi - c_lo) / 32;  // 4 (M = 256) or 2 (M = 128)
       if (lane < nrows && sub0 < nsub) {
         const long long o = static_cast<long long>(rbase + lane) * ep.part_ld + sub0;
-        if (sub0 + kSubs <= nsub) {
+        if (my_subs == 2) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+            if (sub0 + kk < nsub) {
+              ep.part_m[o + kk] = sub_m[kk];
+              ep.part_s[o + kk] = sub_s[kk];
+              ep.part_arg[o + kk] = sub_a[kk];
+            }
+        } else if (sub0 + kSubs <= nsub) {
           *reinterpret_cast<float4*>(ep.part_m + o) =
               make_float4(sub_m[0], sub_m[1], sub_m[2], sub_m[3]);
           *reinterpret_cast<float4*>(ep.part_s + o) =
