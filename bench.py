@@ -138,7 +138,7 @@ class ClockSampler:
                           if r[5 + i].strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
-                "samples": len(sm)}
+                "samples": len(sm), "window": "warm-up + timed steps (100 ms period)"}
 
 
 def run_gpu(args):
@@ -163,6 +163,10 @@ def run_gpu(args):
         if world > 1:
             torch.distributed.barrier()
 
+    # nvidia-smi needs ~0.1-0.2 s to start sampling and a 5-step region lasts
+    # ~70-110 ms, so the sampler runs from the first warm-up step (same load)
+    # through the timed steps.
+    clocks = ClockSampler(local).__enter__()
     for _ in range(max(args.warmup, 3)):
         model.run_staged(cfg)
     torch.cuda.synchronize()
@@ -172,7 +176,7 @@ def run_gpu(args):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with clocks:
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(float(k))
