@@ -166,17 +166,16 @@ def run_gpu(args):
     # nvidia-smi needs ~0.1-0.2 s to start sampling and a 5-step region lasts
     # ~70-110 ms, so the sampler runs from the first warm-up step (same load)
     # through the timed steps.
-    clocks = ClockSampler(local).__enter__()
-    for _ in range(max(args.warmup, 3)):
-        model.run_staged(cfg)
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for _ in range(max(args.warmup, 3)):
+            model.run_staged(cfg)
+        torch.cuda.synchronize()
 
-    # ---- device-resident timed region ----
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize()
-    with clocks:
+        # ---- device-resident timed region ----
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize()
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(float(k))
