@@ -107,6 +107,25 @@ class GpuExecutor {
   }
   void save(const std::string& path) const { check(mtg_model_save(m_, path.c_str())); }
 
+  // encode_infer(embed_source_infer(src, factors)) (model.cpp:539-596): the
+  // encoder output rows [|src| x d_model], row-major.
+  std::vector<float> encode(const std::vector<int>& src,
+                            const std::vector<std::vector<int>>& factor_ids = {}) const {
+    const int64_t off[2] = {0, static_cast<int64_t>(src.size())};
+    const std::string cfg = config_json();
+    const auto p = cfg.find("\"d_model\":");
+    const int d = std::stoi(cfg.substr(p + 10));
+    std::vector<int32_t> block;
+    for (const auto& f : factor_ids) {
+      if (f.size() != src.size()) throw ShapeError("embed_source: factor stream not aligned with words");
+      block.insert(block.end(), f.begin(), f.end());
+    }
+    std::vector<float> out(src.size() * static_cast<size_t>(d));
+    check(mtg_encode_factors(m_, src.data(), off, 1, block.empty() ? nullptr : block.data(),
+                             static_cast<int>(factor_ids.size()), out.data()));
+    return out;
+  }
+
   // decode_step along a forced prefix (model.cpp:614-672): logits per step.
   std::vector<float> forced_logits(const std::vector<int>& src,
                                    const std::vector<int>& forced) const {
@@ -207,6 +226,18 @@ inline Hypothesis beam_search(const GpuExecutor& ex, const std::vector<int>& src
                               const std::vector<int>* shortlist = nullptr) {
   if (config.beam_size < 1) throw UsageError("beam_search: beam size >= 1");
   if (src_ids.empty()) throw UsageError("beam_search: empty source");
+  if (config.max_len <= 0) {
+    // decode.cpp:48-108 with max_len <= 0: the source is still encoded (its
+    // checks throw as in the reference), no search step runs, and the
+    // unfinished root hypothesis comes back truncated. (The C ABI's
+    // max_len <= 0 means "derive 2|src|+5", which is translate_one's rule,
+    // decode.cpp:352-355, not beam_search's.)
+    ex.encode(src_ids, factor_ids);
+    Hypothesis root;
+    root.truncated = true;
+    root.normalized = root.normalized_score(config.length_penalty_alpha);
+    return root;
+  }
   const FactorStreams fs{factor_ids};
   const std::vector<std::vector<int>> sl{shortlist ? *shortlist : std::vector<int>{}};
   BatchResult r = translate_ids(ex, {src_ids}, config, 0, &fs, shortlist ? &sl : nullptr);

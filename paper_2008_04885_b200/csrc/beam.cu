@@ -105,13 +105,8 @@ void launch_beam_init(const BeamDev& b, cudaStream_t st) {
 
 void launch_beam_select(const BeamDev& b, cudaStream_t st) {
   const size_t smem = sizeof(int) * 2 * static_cast<size_t>(b.N);
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
-    MTG_CUDA(cudaFuncSetAttribute(beam_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
+  ensure_smem_attr(beam_select_kernel, smem);
   launch_k(beam_select_kernel, (b.N + kSelWarps - 1) / kSelWarps, kSelWarps * 32, smem, st, b);
   MTG_CUDA(cudaGetLastError());
 }

@@ -52,8 +52,15 @@ void upload_f32_operand(const std::vector<float>& kmaj, int n, int k, int prec, 
 
 // Builds a [N x K] K-major weight from reference tensors. `nt`: tensors are
 // already [rows = N x cols = K] (tgt_embed); otherwise [K x N] (y = x.W).
+// Fragment-order copy of a weight for the small-batch GEMV path (gemv.cuh).
+void build_gemv_copy(DevLinear& L, const void* src, int elem, cudaStream_t st) {
+  L.frag.resize(static_cast<size_t>(gemv_pack_bytes(L.n, L.k_pad, elem)));
+  launch_gemv_pack(src, L.n, L.k_pad, elem, L.frag.get(), st);
+  MTG_CUDA(cudaStreamSynchronize(st));
+}
+
 void build_linear(DevLinear& L, const std::vector<const HostTensor*>& parts, bool nt, int prec,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool gemv_copy = false) {
   const int k = static_cast<int>(nt ? parts[0]->cols() : parts[0]->rows());
   int n = 0;
   for (auto* p : parts) n += static_cast<int>(nt ? p->rows() : p->cols());
@@ -91,6 +98,7 @@ void build_linear(DevLinear& L, const std::vector<const HostTensor*>& parts, boo
     }
     L.q.resize(buf.size());
     L.q.upload(buf.data(), buf.size());
+    if (gemv_copy) build_gemv_copy(L, L.q.get(), 1, st);
   } else {
     std::vector<float> kmaj(size_t(n) * k);
     int n0 = 0;
@@ -107,6 +115,17 @@ void build_linear(DevLinear& L, const std::vector<const HostTensor*>& parts, boo
       n0 += pn;
     }
     upload_f32_operand(kmaj, n, k, prec, L, st);
+    if (gemv_copy && prec == kBF16) {
+      build_gemv_copy(L, L.h.get(), 2, st);
+    } else if (gemv_copy) {  // plain fp32 rows (the GEMV splits them into tf32 hi + lo)
+      std::vector<float> padded(size_t(n) * L.k_pad, 0.0f);
+      for (int j = 0; j < n; ++j)
+        std::copy(kmaj.begin() + size_t(j) * k, kmaj.begin() + size_t(j + 1) * k,
+                  padded.begin() + size_t(j) * L.k_pad);
+      DeviceBuffer<float> f(padded.size());
+      f.upload(padded.data(), padded.size());
+      build_gemv_copy(L, f.get(), 4, st);
+    }
   }
 }
 
@@ -114,13 +133,6 @@ void upload_vec(DeviceBuffer<float>& dst, const HostTensor& t) {
   dst.resize(t.f32.size());
   dst.upload(t.f32.data(), t.f32.size());
 }
-
-struct PlanKey {
-  const void* a;
-  const void* b;
-  int m;
-  bool operator<(const PlanKey& o) const { return std::tie(a, b, m) < std::tie(o.a, o.b, o.m); }
-};
 
 }  // namespace
 
@@ -198,13 +210,12 @@ static int dec_force_bn(int n, int k) {
   return pos == std::string::npos ? 0 : std::atoi(map.c_str() + pos + key.size());
 }
 
-static std::map<PlanKey, GemmPlan>& plan_cache(const void* engine) {
-  static std::map<const void*, std::map<PlanKey, GemmPlan>> caches;
-  auto& c = caches[engine];
+// Per-engine GEMM plans (tensor maps + tiling), used under the engine mutex.
+std::map<Engine::PlanKey, GemmPlan>& Engine::plan_cache() {
   // Plans are keyed by row count; a ragged corpus brings a new one nearly
   // every batch. Graphs copy the tensor maps at capture, so dropping is safe.
-  if (c.size() >= 8192) c.clear();
-  return c;
+  if (plans_.size() >= 8192) plans_.clear();
+  return plans_;
 }
 
 Engine::Engine(HostModel model, int precision, int device)
@@ -222,7 +233,7 @@ Engine::Engine(HostModel model, int precision, int device)
   int ndev = 0;
   MTG_CUDA(cudaGetDeviceCount(&ndev));
   if (device_ < 0 || device_ >= ndev) fail(kUsageError, "bad device id " + std::to_string(device_));
-  MTG_CUDA(cudaSetDevice(device_));
+  DeviceGuard guard(device_);
   MTG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   MTG_CUDA(cudaMallocHost(&h_pinned_, 16 * sizeof(int)));
   d_ = c.d_model;
@@ -236,10 +247,12 @@ Engine::Engine(HostModel model, int precision, int device)
 }
 
 Engine::~Engine() {
+  int prev = -1;
+  cudaGetDevice(&prev);
   cudaSetDevice(device_);
   diag_clear();
   clear_enc_graphs();
-  plan_cache(this).clear();
+  plan_cache().clear();
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (multi_exec_) cudaGraphExecDestroy(multi_exec_);
   if (loop_exec_) cudaGraphExecDestroy(loop_exec_);
@@ -247,6 +260,7 @@ Engine::~Engine() {
   if (h_pinned_) cudaFreeHost(h_pinned_);
   if (res_host_) cudaFreeHost(res_host_);
   if (stream_) cudaStreamDestroy(stream_);
+  if (prev >= 0 && prev != device_) cudaSetDevice(prev);
 }
 
 void Engine::upload_weights() {
@@ -277,7 +291,7 @@ void Engine::upload_weights() {
   } else {
     upload_vec(tgt_embed_f32_, te);
   }
-  build_linear(logits_w_, {&te}, true, prec_, stream_);
+  build_linear(logits_w_, {&te}, true, prec_, stream_, true);
   auto ln = [&](LN& l, const std::string& p) {
     upload_vec(l.g, P(p + ".gain"));
     upload_vec(l.b, P(p + ".bias"));
@@ -307,13 +321,13 @@ void Engine::upload_weights() {
     ln(L.n2, p + ".norm2");
     ln(L.n3, p + ".norm3");
     build_linear(L.self_qkv, {&P(p + ".self.wq"), &P(p + ".self.wk"), &P(p + ".self.wv")}, false,
-                 prec_, stream_);
-    build_linear(L.self_wo, {&P(p + ".self.wo")}, false, prec_, stream_);
-    build_linear(L.cross_q, {&P(p + ".cross.wq")}, false, prec_, stream_);
+                 prec_, stream_, true);
+    build_linear(L.self_wo, {&P(p + ".self.wo")}, false, prec_, stream_, true);
+    build_linear(L.cross_q, {&P(p + ".cross.wq")}, false, prec_, stream_, true);
     build_linear(L.cross_kv, {&P(p + ".cross.wk"), &P(p + ".cross.wv")}, false, prec_, stream_);
-    build_linear(L.cross_wo, {&P(p + ".cross.wo")}, false, prec_, stream_);
-    build_linear(L.w1, {&P(p + ".ffn.w1")}, false, prec_, stream_);
-    build_linear(L.w2, {&P(p + ".ffn.w2")}, false, prec_, stream_);
+    build_linear(L.cross_wo, {&P(p + ".cross.wo")}, false, prec_, stream_, true);
+    build_linear(L.w1, {&P(p + ".ffn.w1")}, false, prec_, stream_, true);
+    build_linear(L.w2, {&P(p + ".ffn.w2")}, false, prec_, stream_, true);
     upload_vec(L.b1, P(p + ".ffn.b1"));
     upload_vec(L.b2, P(p + ".ffn.b2"));
   }
@@ -347,7 +361,7 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
           m_enc, std::min(2 * cap_enc_, cap_sent_ * std::max(host_.config.max_seq_len, 1)));
   }
   cap_beam_ = std::max(beam, cap_beam_);
-  plan_cache(this).clear();
+  plan_cache().clear();
   clear_enc_graphs();
   ++ws_gen_;
   const ModelConfig& c = host_.config;
@@ -485,7 +499,7 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
                   long long ldc, const float* bias, const float* residual, int relu,
                   long long c_step_stride, const int* d_step, unsigned* seg_absmax,
                   float* c_lo) {
-  auto& cache = plan_cache(this);
+  auto& cache = plan_cache();
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
   if (it == cache.end())
@@ -617,7 +631,7 @@ static int logits_force_bn() {
 }
 
 void Engine::gemm_logits(int m, const int* d_m) {
-  auto& cache = plan_cache(this);
+  auto& cache = plan_cache();
   ActOperand& la = logits_act();
   PlanKey key{la.op().ptr, logits_w_.op().ptr, m};
   auto it = cache.find(key);
@@ -942,7 +956,167 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     gemm(act_d_, dec_[l].cross_kv, m, nullptr, ckv_[l].get(), 2 * d, nullptr, nullptr, 0);
 }
 
+bool Engine::small_path() const {
+  static const bool enabled = [] {
+    const char* e = std::getenv("MTG_SMALL_BATCH");
+    return !(e && e[0] == '0');
+  }();
+  return enabled && r_max_ <= kGemvRows && d_ <= 512 && !use_shortlist_;
+}
+
+GemvArgs Engine::gemv_args(const DevLinear& w) const {
+  GemvArgs g;
+  g.d_rows = n_rows_.get();
+  g.rows_alloc = std::min(r_max_, kGemvRows);
+  g.d_step = step_.get();
+  g.K = w.k;
+  g.k_pad = w.k_pad;
+  g.N = w.n;
+  g.w = w.frag.get();
+  if (!g.w) fail(kStateError, "gemv: fragment-order weight copy missing");
+  g.w_seg_scale = w.seg_scale.get();
+  g.seg_width = w.seg_width;
+  g.nonfinite = nonfinite_.get();
+  return g;
+}
+
+// decode_step (model.cpp:614-672) for <= kGemvRows live rows: per decoder
+// layer QKV, self-attention, Wo(+res), cross-Wq, cross-attention,
+// cross-Wo(+res), W1(+b1, ReLU), W2(+b2, res); the LayerNorms, the target
+// embedding (+ history reorder) and every int8 row quantization run inside
+// the consuming GEMV, so a step is 8 kernels per layer + projection + tail.
+void Engine::decoder_body_small(bool reorder) {
+  const ModelConfig& c = host_.config;
+  const long long d = d_;
+  const int R = r_max_;
+  const int* dr = n_rows_.get();
+  const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
+  const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
+  const int gp = prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2;
+  OperandOut none;
+  none.prec = -1;  // attention writes the fp32 context only
+  static const bool small_attn_env = [] {
+    const char* e = std::getenv("MTG_SMALL_ATTN");
+    return !(e && e[0] == '0');
+  }();
+  const bool small_attn = small_attn_env && attn_small_supported(d_, heads_, T_, T_);
+  auto set_start = [&](GemvArgs& g) {  // first consumer of the step: embedding + reorder
+    g.a_mode = 2;
+    g.prev = row_prev_.get();
+    g.table = tgt_embed_f32_.get();  // int8: q / scale, dequantized at load
+    g.table_rows = V_;
+    g.pe = pe_.get();
+    g.sqrt_d = sqrt_d;
+    g.x_out = dec_y_.get();
+    g.ldx_out = d;
+    g.reorder = reorder ? 1 : 0;
+    g.row_parent = row_parent_.get();
+    g.anc[0] = anc0_.get();
+    g.anc[1] = anc1_.get();
+    g.tok[0] = tok0_.get();
+    g.tok[1] = tok1_.get();
+    g.T = T_;
+  };
+  auto ln_from = [&](GemvArgs& g, const LN& ln) {
+    g.a_mode = 1;
+    g.x = dec_y_.get();
+    g.ldx = d;
+    g.ln_g = ln.g.get();
+    g.ln_b = ln.b.get();
+  };
+  auto rows_from = [&](GemvArgs& g, const float* x, long long ldx) {
+    g.a_mode = 0;
+    g.x = x;
+    g.ldx = ldx;
+  };
+  auto out_to = [&](GemvArgs& g, float* C, long long ldc, const float* bias, bool res, int relu) {
+    g.C = C;
+    g.ldc = ldc;
+    g.bias = bias;
+    g.residual = res ? C : nullptr;
+    g.ldr = ldc;
+    g.relu = relu;
+  };
+  for (int l = 0; l < c.num_decoder_layers; ++l) {
+    DecLayer& L = dec_[l];
+    GemvArgs q = gemv_args(L.self_qkv);
+    if (l == 0) set_start(q);
+    q.x = dec_y_.get();  // a_mode 2 ignores x; LayerNorm params below
+    q.ldx = d;
+    if (l > 0) ln_from(q, L.n1);
+    q.ln_g = L.n1.g.get();
+    q.ln_b = L.n1.b.get();
+    out_to(q, qkv_cache_[l].get(), 3 * d, nullptr, false, 0);
+    q.c_step_stride = static_cast<long long>(R) * 3 * d;
+    launch_gemv(gp, false, q, stream_);
+    count(l == 0 ? "gemv qkv (+embed, LN)" : "gemv qkv (+LN)");
+    if (small_attn) {
+      launch_attn_small_self(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(),
+                             row_parent_.get(), reorder ? 1 : 0, dr, step_.get(),
+                             std::min(R, kGemvRows), d_, heads_, scale, dec_ctx_.get(), d, stream_);
+    } else {
+      launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
+                                step_.get(), d_, heads_, scale, dec_ctx_.get(), d, none, stream_);
+    }
+    count("self attention");
+    GemvArgs o = gemv_args(L.self_wo);
+    rows_from(o, dec_ctx_.get(), d);
+    out_to(o, dec_y_.get(), d, nullptr, true, 0);
+    launch_gemv(gp, false, o, stream_);
+    count("gemv wo (+res)");
+    GemvArgs cq = gemv_args(L.cross_q);
+    ln_from(cq, L.n2);
+    out_to(cq, dec_cq_.get(), d, nullptr, false, 0);
+    launch_gemv(gp, false, cq, stream_);
+    count("gemv cross wq (+LN)");
+    if (small_attn) {
+      launch_attn_small_cross(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
+                              enc_len_.get(), dr, std::min(R, kGemvRows), T_, d_, heads_, scale,
+                              dec_ctx_.get(), d, stream_);
+    } else {
+      launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
+                                 enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d,
+                                 none, stream_);
+    }
+    count("cross attention");
+    GemvArgs co = gemv_args(L.cross_wo);
+    rows_from(co, dec_ctx_.get(), d);
+    out_to(co, dec_y_.get(), d, nullptr, true, 0);
+    launch_gemv(gp, false, co, stream_);
+    count("gemv cross wo (+res)");
+    GemvArgs f1 = gemv_args(L.w1);
+    ln_from(f1, L.n3);
+    out_to(f1, ffh_.get(), dff_, L.b1.get(), false, 1);
+    launch_gemv(gp, false, f1, stream_);
+    count("gemv w1 (+LN, b1, relu)");
+    GemvArgs f2 = gemv_args(L.w2);
+    rows_from(f2, ffh_.get(), dff_);
+    out_to(f2, dec_y_.get(), d, L.b2.get(), true, 0);
+    launch_gemv(gp, false, f2, stream_);
+    count("gemv w2 (+b2, res)");
+  }
+  GemvArgs lg = gemv_args(logits_w_);
+  if (c.num_decoder_layers == 0) set_start(lg);
+  else ln_from(lg, dec_final_);
+  lg.x = dec_y_.get();
+  lg.ldx = d;
+  lg.ln_g = dec_final_.g.get();
+  lg.ln_b = dec_final_.b.get();
+  lg.C = logits_.get();
+  lg.ldc = Vp_;
+  lg.part_m = part_m_.get();
+  lg.part_s = part_s_.get();
+  lg.part_arg = part_arg_.get();
+  lg.part_ld = part_ld_;
+  launch_gemv(gp, true, lg, stream_);
+  count("gemv logits + softmax partials (+LN)");
+}
+
 void Engine::decoder_body(bool reorder) {
+  if (small_path()) {
+    decoder_body_small(reorder);
+    return;
+  }
   const ModelConfig& c = host_.config;
   const long long d = d_;
   const int R = r_max_;
@@ -1246,6 +1420,7 @@ std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vecto
                                                     const BeamConfigC& cfg,
                                                     const FactorStreams* factors,
                                                     const std::vector<std::vector<int>>* shortlists) {
+  DeviceGuard guard(device_);
   stage(srcs, factors, shortlists);
   run_staged(cfg);
   const int n = staged_n_;
@@ -1294,11 +1469,29 @@ std::vector<SentenceResult> Engine::translate_batch(const std::vector<std::vecto
     r.logprob = lp[s];
     r.norm = norm[s];
   }
+  if (bad && n > 1) {
+    // A non-finite quantize input (quant.cpp:110-112) fails only the sentence
+    // it came from (translate_corpus, decode.cpp:403-410). The device flag is
+    // per batch, so the batch's sentences are re-decoded one by one: their
+    // results do not depend on the batch composition (every quantization
+    // segment is a sentence or one of its rows).
+    const std::vector<int> status0 = staged_status_;
+    for (int s = 0; s < n; ++s) {
+      if (status0[s]) continue;
+      FactorStreams fs1;
+      if (factors) fs1.push_back((*factors)[s]);
+      std::vector<std::vector<int>> sl1;
+      if (shortlists) sl1.push_back((*shortlists)[s]);
+      out[s] = translate_batch({srcs[s]}, cfg, factors ? &fs1 : nullptr,
+                               shortlists ? &sl1 : nullptr)[0];
+    }
+  }
   return out;
 }
 
 void Engine::stage(const std::vector<std::vector<int>>& srcs, const FactorStreams* factors,
                    const std::vector<std::vector<int>>* shortlists) {
+  DeviceGuard guard(device_);
   const int n = static_cast<int>(srcs.size());
   if (factors && static_cast<int>(factors->size()) != n)
     fail(kShapeError, "factor streams: one entry per sentence");
@@ -1344,6 +1537,7 @@ void Engine::stage(const std::vector<std::vector<int>>& srcs, const FactorStream
 }
 
 void Engine::run_staged(const BeamConfigC& cfg) {
+  DeviceGuard guard(device_);
   if (cfg.beam_size < 1) fail(kUsageError, "beam_search: beam size >= 1");
   if (cfg.beam_size > kMaxBeam)
     fail(kUsageError, "beam size above " + std::to_string(kMaxBeam) + " is not supported");
@@ -1379,6 +1573,7 @@ void Engine::run_staged(const BeamConfigC& cfg) {
 }
 
 void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double* flops) {
+  DeviceGuard guard(device_);
   if (staged_n_ == 0 || last_beam_ == 0)
     fail(kStateError, "time_kernel: stage a batch and run it once first");
   if (iters < 1) fail(kUsageError, "time_kernel: iters >= 1");
@@ -1429,6 +1624,117 @@ void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double
     *bytes = double(split) * eb * (double(dff_) * enc_[0].w1.k_pad + double(M) * act_d_.k_pad) +
              4.0 * M * dff_;
     *flops = 2.0 * M * dff_ * d_ * (prec_ == kF32 ? 3 : 1);
+  } else if (kernel >= 10 && kernel <= 17) {
+    // Small-batch step pieces, each chained `iters` times inside one CUDA
+    // graph with PDL (the in-graph cost of one dependent launch).
+    if (!small_path()) fail(kStateError, "time_kernel: the staged batch does not use the GEMV step");
+    const int t = std::max(0, last_t_run_ - 1);
+    n_rows_.upload(&R, 1, stream_);
+    step_.upload(&t, 1, stream_);
+    const int gp = prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2;
+    const long long d = d_;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
+    OperandOut none;
+    none.prec = -1;
+    DecLayer& L = dec_.at(0);
+    std::function<void()> one;
+    if (kernel == 10) {  // empty dependent kernel: the launch / PDL floor
+      one = [&] { launch_noop(stream_); };
+      *bytes = 0.0;
+    } else if (kernel == 11) {  // Wo GEMV + residual
+      one = [&] {
+        GemvArgs o = gemv_args(L.self_wo);
+        o.x = dec_ctx_.get();
+        o.ldx = d;
+        o.C = dec_y_.get();
+        o.ldc = d;
+        o.residual = dec_y_.get();
+        o.ldr = d;
+        launch_gemv(gp, false, o, stream_);
+      };
+      *bytes = double(L.self_wo.n) * L.self_wo.k_pad * prec_elem_bytes(gemm_prec_of(prec_));
+    } else if (kernel == 12) {  // LayerNorm + W1 GEMV + bias + ReLU
+      one = [&] {
+        GemvArgs f1 = gemv_args(L.w1);
+        f1.a_mode = 1;
+        f1.x = dec_y_.get();
+        f1.ldx = d;
+        f1.ln_g = L.n3.g.get();
+        f1.ln_b = L.n3.b.get();
+        f1.C = ffh_.get();
+        f1.ldc = dff_;
+        f1.bias = L.b1.get();
+        f1.relu = 1;
+        launch_gemv(gp, false, f1, stream_);
+      };
+      *bytes = double(L.w1.n) * L.w1.k_pad * prec_elem_bytes(gemm_prec_of(prec_));
+    } else if (kernel == 13) {  // final LayerNorm + output projection + partials
+      one = [&] {
+        GemvArgs lg = gemv_args(logits_w_);
+        lg.a_mode = 1;
+        lg.x = dec_y_.get();
+        lg.ldx = d;
+        lg.ln_g = dec_final_.g.get();
+        lg.ln_b = dec_final_.b.get();
+        lg.C = logits_.get();
+        lg.ldc = Vp_;
+        lg.part_m = part_m_.get();
+        lg.part_s = part_s_.get();
+        lg.part_arg = part_arg_.get();
+        lg.part_ld = part_ld_;
+        launch_gemv(gp, true, lg, stream_);
+      };
+      *bytes = double(logits_w_.n) * logits_w_.k_pad * prec_elem_bytes(gemm_prec_of(prec_));
+    } else if (kernel == 14) {  // decoder self-attention at the last step
+      one = [&, scale] {
+        launch_dec_self_attention(qkv_cache_[0].get(), r_max_, T_, anc0_.get(), anc1_.get(),
+                                  n_rows_.get(), step_.get(), d_, heads_, scale, dec_ctx_.get(),
+                                  d_, none, stream_);
+      };
+      *bytes = 4.0 * R * (double(t + 1) * 2 * d_);
+    } else if (kernel == 16) {  // small-batch self-attention (attn_small.cu)
+      one = [&, scale] {
+        launch_attn_small_self(qkv_cache_[0].get(), r_max_, T_, anc0_.get(), anc1_.get(),
+                               row_parent_.get(), 1, n_rows_.get(), step_.get(),
+                               std::min(r_max_, kGemvRows), d_, heads_, scale, dec_ctx_.get(), d_,
+                               stream_);
+      };
+      *bytes = 4.0 * R * (double(t + 1) * 2 * d_);
+    } else if (kernel == 17) {  // small-batch cross-attention
+      one = [&, scale] {
+        launch_attn_small_cross(dec_cq_.get(), d_, ckv_[0].get(), row_sent_.get(), enc_off_.get(),
+                                enc_len_.get(), n_rows_.get(), std::min(r_max_, kGemvRows), T_, d_,
+                                heads_, scale, dec_ctx_.get(), d_, stream_);
+      };
+      *bytes = 4.0 * R * (double(staged_max_src_) * 2 * d_);
+    } else {  // log-softmax / top-k merge over the live rows
+      one = [&] {
+        launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
+                            part_ld_, beam_, stream_);
+      };
+      *bytes = 12.0 * R * ((V_ + 31) / 32);
+    }
+    *flops = 0.0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    MTG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) one();
+    MTG_CUDA(cudaStreamEndCapture(stream_, &g));
+    MTG_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    launch = [&] { MTG_CUDA(cudaGraphLaunch(ge, stream_)); };
+    launch();  // warm
+    MTG_CUDA(cudaEventRecord(e0, stream_));
+    launch();
+    MTG_CUDA(cudaEventRecord(e1, stream_));
+    MTG_CUDA(cudaEventSynchronize(e1));
+    float total = 0.0f;
+    MTG_CUDA(cudaEventElapsedTime(&total, e0, e1));
+    *ms = total / iters;
+    cudaGraphExecDestroy(ge);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return;
   } else {
     fail(kUsageError, "time_kernel: unknown kernel id");
   }
@@ -1446,6 +1752,7 @@ void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double
 
 void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int* forced, int nf,
                            float* out, const FactorStreams* factors) {
+  DeviceGuard guard(device_);
   const int n = static_cast<int>(srcs.size());
   if (n == 0 || nf <= 0) return;
   stage(srcs, factors);
@@ -1488,6 +1795,7 @@ void Engine::forced_logits(const std::vector<std::vector<int>>& srcs, const int*
 
 void Engine::encode(const std::vector<std::vector<int>>& srcs, float* out,
                     const FactorStreams* factors) {
+  DeviceGuard guard(device_);
   const int n = static_cast<int>(srcs.size());
   if (n == 0) return;
   stage(srcs, factors);

@@ -17,6 +17,7 @@
 
 #include "device_buffer.hpp"
 #include "gemm.hpp"
+#include "gemv.cuh"
 #include "kernels.cuh"
 #include "model_host.hpp"
 
@@ -31,6 +32,7 @@ struct DevLinear {
   DeviceBuffer<int8_t> q;
   DeviceBuffer<__nv_bfloat16> h;
   DeviceBuffer<float> hi, lo;
+  DeviceBuffer<uint8_t> frag;     // small-batch GEMV copy in mma fragment order (gemv.cuh)
   DeviceBuffer<float> seg_scale;  // int8: weight scale per fused segment
   int seg_width = 0;              // columns per segment (0: one segment)
   Operand op() const;
@@ -122,11 +124,25 @@ class Engine {
   void run_encoder_body(int n_sent, int m_enc, int max_src);
   // reorder: beam search (copy histories from row_parent at step >= 1).
   void decoder_body(bool reorder);  // decoder layers + dec_final + logits for the live rows
+  // Small batches (<= kGemvRows live rows): the step as GEMV kernels with the
+  // LayerNorms / quantization folded into the consumers (gemv.cuh).
+  bool small_path() const;
+  void decoder_body_small(bool reorder);
+  GemvArgs gemv_args(const DevLinear& w) const;
   void decode_loop(int t_run);
   // Launch accounting; with MTG_DIAG_EVENTS=1 the step graph also records an
   // event after every kernel (breaks PDL overlap -- diagnostics only) and
   // decode_loop accumulates per-kernel times for diag_report().
   void count(const char* tag = "kernel");
+
+  struct PlanKey {
+    const void* a;
+    const void* b;
+    int m;
+    bool operator<(const PlanKey& o) const { return std::tie(a, b, m) < std::tie(o.a, o.b, o.m); }
+  };
+  std::map<PlanKey, GemmPlan> plans_;
+  std::map<PlanKey, GemmPlan>& plan_cache();
 
   HostModel host_;
   int prec_;

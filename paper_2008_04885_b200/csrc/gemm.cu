@@ -53,12 +53,7 @@ CUtensorMap make_map(const void* ptr, int prec, int rows, int k_pad, int box_row
 
 template <int PREC, int BN, int EPI, int FL = -1>
 void launch_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    MTG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<PREC, BN, EPI, FL>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  ensure_smem_attr(gemm_tc_kernel<PREC, BN, EPI, FL>, 227 * 1024);
   dim3 grid(p.n_tiles, p.m_tiles, p.splits);
   if (p.splits > 1) {  // split-K: the z splits of a tile form one cluster
     cudaLaunchConfig_t cfg{};
@@ -242,12 +237,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
 namespace {
 template <int PREC, int BN, int EG>
 void launch_logits_one(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    MTG_CUDA(cudaFuncSetAttribute(logits_tc_kernel<PREC, BN, EG>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  ensure_smem_attr(logits_tc_kernel<PREC, BN, EG>, 227 * 1024);
   const int grid = std::min(148, p.m_tiles * p.n_tiles);
   launch_k(logits_tc_kernel<PREC, BN, EG>, grid, 64 + EG * 256, p.smem, stream, p.a, p.b, p.a2,
            p.b2, p.num_kb, p.nst, p.n_tiles, ep);
@@ -313,12 +303,7 @@ GemmPlan plan_logits_pair(const Operand& a, const Operand& b, int m_max, int n) 
 }
 
 static void launch_logits_pair(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    MTG_CUDA(cudaFuncSetAttribute(logits_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    configured = true;
-  }
+  ensure_smem_attr(logits_tc2_kernel, 227 * 1024);
   if (!ep.part_m) fail(kStateError, "logits: softmax partial buffers missing");
   if (ep.part_ld % 4 != 0 || ep.part_ld * 32 < ep.N)
     fail(kStateError, "logits pair: softmax partial pitch");

@@ -1,0 +1,467 @@
+// Small-batch decode GEMVs (gemv.cuh): weights prefetched by bulk copies
+// before the PDL wait, operand (LayerNorm / embedding / int8 quantization)
+// built per CTA, warp-per-output dot products, reference epilogues.
+#include "gemv.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include <cuda_bf16.h>
+
+#include "detmath.cuh"
+#include "errors.hpp"
+#include "launch.cuh"
+#include "ptx.cuh"
+#include "rowops.cuh"
+
+namespace mtg {
+
+namespace {
+
+constexpr int kGemvThreads = 256;
+constexpr int kGemvWarps = kGemvThreads / 32;
+constexpr int kMaxGemvStages = 4;
+constexpr int kLnKpl = 16;       // LayerNorm rows of d <= 512 in registers
+constexpr int kKStepBytes = 32;  // one mma K step: 32 int8 / 16 bf16 / 8 tf32 elements
+#define kNegInfF (-__int_as_float(0x7f800000))
+
+template <int PREC>
+struct GemvElem {
+  static constexpr int bytes = PREC == 0 ? 1 : PREC == 1 ? 2 : 4;
+};
+
+// Shared-memory carve-up (bytes), identical on host and device. Weight
+// chunks arrive in fragment order (launch_gemv_pack); the operand rows are
+// written in B-fragment order ([K step][lane][b0, b1]).
+struct GemvSmem {
+  int stage_bytes, nst, a_off, part_off, scale_off, ex_off, bar_off, total;
+};
+__host__ __device__ inline GemvSmem gemv_smem(int chunk, int ks, int row_bytes, int nst) {
+  GemvSmem s;
+  s.stage_bytes = (chunk * row_bytes + 127) / 128 * 128;
+  s.nst = nst;
+  s.a_off = nst * s.stage_bytes;
+  s.part_off = s.a_off + kGemvRows * row_bytes;
+  s.scale_off = s.part_off + ks * kGemvRows * chunk * 4;
+  s.ex_off = s.scale_off + kGemvRows * 4 * 4;  // [8 rows][4 segments] int8 epilogue factors
+  s.bar_off = (s.ex_off + kGemvWarps * 32 * 4 + 7) / 8 * 8;
+  s.total = s.bar_off + kMaxGemvStages * 8;
+  return s;
+}
+
+// Byte offset of operand element (row n, K byte offset o) in the B-fragment
+// block: K step o / 32, register (o % 32) / 16, lane n * 4 + (o % 16) / 4.
+__device__ __forceinline__ int bfrag_off(int n, int o) {
+  return ((o >> 5) * 32 + n * 4 + ((o & 15) >> 2)) * 8 + ((o >> 4) & 1) * 4 + (o & 3);
+}
+
+__device__ __forceinline__ uint32_t tf32_hi(uint32_t x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(__uint_as_float(x)));
+  return h;
+}
+
+// D += A (16 weight rows x 1 K step) . B (1 K step x 8 operand rows), the
+// registers loaded from the fragment-order blocks (PTX mma.sync layouts:
+// a0/a2 row g, a1/a3 row g + 8 at K bytes 4q / 16 + 4q; b0/b1 operand row g).
+template <int PREC>
+__device__ __forceinline__ void mma_step(uint32_t (&d)[4], const uint8_t* wf, const uint8_t* xf) {
+  const uint4 av = *reinterpret_cast<const uint4*>(wf);
+  const uint2 bv = *reinterpret_cast<const uint2*>(xf);
+  uint32_t a[4] = {av.x, av.y, av.z, av.w};
+  uint32_t b[2] = {bv.x, bv.y};
+  if constexpr (PREC == 0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  } else if constexpr (PREC == 1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  } else {
+    // TF32x3 (as the tcgen05 path): x = hi + lo, acc += lo.hi + hi.lo + hi.hi.
+    uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ah[i] = tf32_hi(a[i]);
+      al[i] = __float_as_uint(__fsub_rn(__uint_as_float(a[i]), __uint_as_float(ah[i])));
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      bh[i] = tf32_hi(b[i]);
+      bl[i] = __float_as_uint(__fsub_rn(__uint_as_float(b[i]), __uint_as_float(bh[i])));
+    }
+#define MTG_MMA_TF32(A, B)                                                                       \
+  asm volatile(                                                                                  \
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "        \
+      "{%8,%9}, {%0,%1,%2,%3};"                                                                  \
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])                                           \
+      : "r"(A[0]), "r"(A[1]), "r"(A[2]), "r"(A[3]), "r"(B[0]), "r"(B[1]))
+    MTG_MMA_TF32(al, bh);
+    MTG_MMA_TF32(ah, bl);
+    MTG_MMA_TF32(ah, bh);
+#undef MTG_MMA_TF32
+  }
+}
+
+// Stores one operand element (value x of row n at column c) into the
+// B-fragment block; int8 already quantized.
+template <int PREC>
+__device__ __forceinline__ void store_elem(uint8_t* A, int n, int c, float x, int8_t q) {
+  constexpr int E = PREC == 0 ? 1 : PREC == 1 ? 2 : 4;
+  uint8_t* p = A + bfrag_off(n, c * E);
+  if constexpr (PREC == 0)
+    *reinterpret_cast<int8_t*>(p) = q;
+  else if constexpr (PREC == 1)
+    *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(x);
+  else
+    *reinterpret_cast<float*>(p) = x;
+}
+
+// Writes row r's operand (values v[i] at column lane + 32 i) into the
+// B-fragment block; int8 with the row's quantization scale.
+template <int PREC, int KPL>
+__device__ __forceinline__ void store_operand_regs(uint8_t* A, int r, const float (&v)[KPL], int n,
+                                                   int k_pad, float scale, int lane) {
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= k_pad) continue;
+    const float x = c < n ? v[i] : 0.0f;
+    store_elem<PREC>(A, r, c, x, c < n && PREC == 0 ? quant1(x, scale) : int8_t(0));
+  }
+  for (int c = 32 * KPL + lane; c < k_pad; c += 32) store_elem<PREC>(A, r, c, 0.0f, 0);
+}
+
+// One CTA processes chunks of `chunk` output columns (weight rows); the 8
+// warps split a chunk into chunk/16 column groups x ks K ranges. Partial
+// sums meet in shared memory and are added in K-range order (int8 exact).
+template <int PREC, bool LOGITS>
+__global__ void __launch_bounds__(kGemvThreads, 1)
+    gemv_kernel(const GemvArgs a, int chunk, int ks, int nst, uint32_t piece) {
+  constexpr int E = GemvElem<PREC>::bytes;
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int row_bytes = a.k_pad * E;
+  const GemvSmem L = gemv_smem(chunk, ks, row_bytes, nst);
+  uint8_t* stages = sm;
+  uint8_t* A = sm + L.a_off;
+  uint32_t* part = reinterpret_cast<uint32_t*>(sm + L.part_off);
+  float* inv = reinterpret_cast<float*>(sm + L.scale_off);  // [r][seg] (int8)
+  float* ex = reinterpret_cast<float*>(sm + L.ex_off);      // [warp][32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.bar_off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_chunks = (a.N + chunk - 1) / chunk;
+  const int G = gridDim.x;
+  const int my_count = static_cast<int>(blockIdx.x) < n_chunks
+                           ? (n_chunks - 1 - static_cast<int>(blockIdx.x)) / G + 1
+                           : 0;
+  const uint8_t* W = static_cast<const uint8_t*>(a.w);
+  // Chunk i of this CTA -> stage i % nst: its 16-row groups are contiguous
+  // in the fragment-order copy, so one bulk copy (issued by one thread).
+  // Issued by warp 0 as `piece`-byte bulk copies spread over its lanes.
+  auto issue = [&](int i) {
+    const int n0 = (blockIdx.x + i * G) * chunk;
+    const int rows = min(chunk, (a.N + 15) / 16 * 16 - n0);
+    const uint32_t bytes = static_cast<uint32_t>(rows) * row_bytes;
+    uint64_t* bar = &full[i % nst];
+    if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+    __syncwarp();
+    uint8_t* dst = stages + (i % nst) * L.stage_bytes;
+    const uint8_t* src = W + static_cast<long long>(n0) * row_bytes;
+    for (uint32_t o = lane * piece; o < bytes; o += 32u * piece)
+      bulk_load(dst + o, src + o, min(piece, bytes - o), bar);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // Everything that does not depend on the previous kernel is fetched before
+  // the programmatic-dependency wait: the weight chunks, LayerNorm gain /
+  // bias, the output bias of this CTA's first chunk, the int8 weight scales.
+  if (warp == 0)
+    for (int i = 0; i < min(nst, my_count); ++i) issue(i);
+  const int r = warp;  // operand row built by this warp
+  const bool ln = a.a_mode != 0;
+  float xv[kLnKpl], gv[kLnKpl], bv[kLnKpl];
+  if (ln) {
+#pragma unroll
+    for (int i = 0; i < kLnKpl; ++i) {
+      const int c = lane + 32 * i;
+      gv[i] = c < a.K ? a.ln_g[c] : 0.0f;
+      bv[i] = c < a.K ? a.ln_b[c] : 0.0f;
+    }
+  }
+  const int n_first = blockIdx.x * chunk;
+  const int ep_r = threadIdx.x / chunk, ep_c = threadIdx.x % chunk;  // first-chunk epilogue slot
+  const bool ep_ok = !LOGITS && my_count > 0 && ep_r < a.rows_alloc && n_first + ep_c < a.N;
+  const float bias0 = ep_ok && a.bias ? a.bias[n_first + ep_c] : 0.0f;
+  const float sw = PREC == 0 && lane < 4 ? a.w_seg_scale[a.seg_width > 0 ? lane : 0] : 1.0f;
+  pdl_wait();
+  pdl_trigger();
+  // Dependent loads, all issued together: live-row count, step, the operand
+  // rows (every allocated row; rows >= R are computed and discarded), the
+  // first chunk's residual.
+  const int R_dev = *a.d_rows;
+  const int t = a.d_step ? *a.d_step : 0;
+  const float res0 = ep_ok && a.residual ? a.residual[ep_r * a.ldr + n_first + ep_c] : 0.0f;
+  const bool have_row = r < a.rows_alloc;
+  if (ln && have_row) {
+    const int n = a.K;
+    if (a.a_mode == 2) {
+      const long long id = min(max(a.prev[r], 0), a.table_rows - 1);
+      const float* pe = a.pe + static_cast<long long>(t) * n;
+#pragma unroll
+      for (int i = 0; i < kLnKpl; ++i) {
+        const int c = lane + 32 * i;
+        xv[i] = c < n ? __fadd_rn(__fmul_rn(a.table[id * n + c], a.sqrt_d), pe[c]) : 0.0f;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kLnKpl; ++i) {
+        const int c = lane + 32 * i;
+        xv[i] = c < n ? a.x[r * a.ldx + c] : 0.0f;
+      }
+    }
+  }
+  const int R = min(R_dev, kGemvRows);
+
+  // ---- step start: beam history reorder (beam.cu beam_reorder_kernel) ----
+  if (a.a_mode == 2 && a.reorder && t >= 1 && blockIdx.x == G - 1) {
+    const int cur = (t - 1) & 1, nxt = t & 1;
+    for (int rr = 0; rr < R; ++rr) {
+      const int pr = a.row_parent[rr];
+      const int* ac = a.anc[cur] + static_cast<long long>(pr) * a.T;
+      int* an = a.anc[nxt] + static_cast<long long>(rr) * a.T;
+      const int* tc = a.tok[cur] + static_cast<long long>(pr) * a.T;
+      int* tn = a.tok[nxt] + static_cast<long long>(rr) * a.T;
+      for (int j = threadIdx.x; j < t && j < a.T; j += blockDim.x) an[j] = ac[j];
+      for (int j = threadIdx.x; j < t - 1; j += blockDim.x) tn[j] = tc[j];
+      if (threadIdx.x == 0) {
+        if (t < a.T) an[t] = rr;
+        if (t - 1 < a.T) tn[t - 1] = a.prev[rr];
+      }
+    }
+  }
+
+  // ---- operand rows: warp r builds row r (rows past the allocation are zero) ----
+  {
+    int bad = 0;
+    float scale = 1.0f;
+    if (!have_row) {
+      for (int c = lane; c < a.k_pad; c += 32) store_elem<PREC>(A, r, c, 0.0f, 0);
+    } else if (ln) {  // LayerNorm (d <= 512) of x or of the target embedding
+      if (a.a_mode == 2 && blockIdx.x == 0 && r < R) {
+#pragma unroll
+        for (int i = 0; i < kLnKpl; ++i)
+          if (lane + 32 * i < a.K) a.x_out[r * a.ldx_out + lane + 32 * i] = xv[i];
+      }
+      const float mx = ln_normalize_regs<kLnKpl>(xv, gv, bv, a.K, lane, &bad);
+      scale = qscale_of(mx);
+      store_operand_regs<PREC, kLnKpl>(A, r, xv, a.K, a.k_pad, scale, lane);
+    } else {  // plain fp32 rows (attention contexts, FFN hidden rows)
+      const float* xr = a.x + r * a.ldx;
+      if constexpr (PREC == 0) {
+        float mx = 0.0f;
+        for (int c = lane; c < a.K; c += 32) {
+          const float v = xr[c];
+          mx = fmaxf(mx, fabsf(v));
+          bad |= !isfinite(v);
+        }
+        scale = qscale_of(warp_allmax(mx));
+      }
+      for (int c = lane; c < a.k_pad; c += 32) {
+        const float v = c < a.K ? xr[c] : 0.0f;
+        store_elem<PREC>(A, r, c, v, PREC == 0 && c < a.K ? quant1(v, scale) : int8_t(0));
+      }
+    }
+    if constexpr (PREC == 0) {
+      // quantize() throws on non-finite input (quant.cpp:110-112)
+      if (r < R && blockIdx.x == 0 && __any_sync(0xffffffffu, bad) && lane == 0)
+        atomicExch(a.nonfinite, 1);
+      // epilogue factor 1 / (sa * sw) per weight segment (quant.cpp:160, 189)
+      if (lane < 4) inv[r * 4 + lane] = __frcp_rn(__fmul_rn(scale, sw));
+    }
+  }
+  __syncthreads();
+
+  const int ksteps = row_bytes / kKStepBytes;
+  const int gi = warp / ks, kr = warp % ks;  // column group, K range
+  const int s_begin = kr * ksteps / ks, s_end = (kr + 1) * ksteps / ks;
+  const int g = lane >> 2, q = lane & 3;
+  const long long step_off = a.c_step_stride ? static_cast<long long>(t) * a.c_step_stride : 0LL;
+  for (int i = 0; i < my_count; ++i) {
+    const int s = i % nst;
+    mbar_wait(&full[s], (i / nst) & 1);
+    const int n0 = (blockIdx.x + i * G) * chunk;
+    const int ncols = min(chunk, a.N - n0);
+    if (gi * 16 < chunk) {
+      // group gi of the chunk: [K step][lane][16 bytes]
+      const uint8_t* wf = stages + s * L.stage_bytes + gi * ksteps * 512 + lane * 16;
+      const uint8_t* xf = A + lane * 8;
+      uint32_t d[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 4
+      for (int st = s_begin; st < s_end; ++st) mma_step<PREC>(d, wf + st * 512, xf + st * 256);
+      uint32_t* pp = part + kr * kGemvRows * chunk;
+      const int c0 = gi * 16 + g;
+      pp[(2 * q) * chunk + c0] = d[0];
+      pp[(2 * q + 1) * chunk + c0] = d[1];
+      pp[(2 * q) * chunk + c0 + 8] = d[2];
+      pp[(2 * q + 1) * chunk + c0 + 8] = d[3];
+    }
+    __syncthreads();  // stage s consumed, partials complete
+    if (warp == 0 && i + nst < my_count) issue(i + nst);
+
+    // Sum of the K-range partials (in order) and the reference epilogue
+    // conversion: int8 float(acc) * (1 / (sa * sw)).
+    auto value = [&](int r, int c) -> float {
+      if constexpr (PREC == 0) {
+        int acc = 0;
+        for (int k = 0; k < ks; ++k) acc += static_cast<int>(part[(k * kGemvRows + r) * chunk + c]);
+        const int n = n0 + c;
+        const int seg = a.seg_width > 0 ? min(n / a.seg_width, 3) : 0;
+        return __fmul_rn(__int2float_rn(acc), inv[r * 4 + seg]);
+      } else {
+        float acc = __uint_as_float(part[r * chunk + c]);
+        for (int k = 1; k < ks; ++k)
+          acc = __fadd_rn(acc, __uint_as_float(part[(k * kGemvRows + r) * chunk + c]));
+        return acc;
+      }
+    };
+    if constexpr (!LOGITS) {
+      for (int idx = threadIdx.x; idx < R * ncols; idx += blockDim.x) {
+        const int rr = idx / ncols, c = idx - rr * ncols, n = n0 + c;
+        // first chunk: bias / residual already in registers (slot == idx)
+        const bool pre = i == 0 && rr == ep_r && c == ep_c;
+        float y = value(rr, c);
+        if (a.bias) y = __fadd_rn(y, pre ? bias0 : a.bias[n]);
+        if (a.relu) y = y > 0.0f ? y : 0.0f;
+        if (a.residual) y = __fadd_rn(pre ? res0 : a.residual[rr * a.ldr + n], y);
+        a.C[step_off + rr * a.ldc + n] = y;
+      }
+    } else {
+      // Output projection: per (32-column slice, row) a warp stores the
+      // logits and the slice partials -- max, first argmax (strict >, so
+      // NaN never wins) and the sequential sum of exp(x - max) in column
+      // order (P6).
+      const int n_sl = (ncols + 31) / 32;
+      float* e = ex + warp * 32;
+      for (int pr = warp; pr < n_sl * R; pr += kGemvWarps) {
+        const int sl = pr / R, rr = pr - sl * R;
+        const int c = sl * 32 + lane;
+        const int nv = min(32, ncols - sl * 32);
+        const bool ok = lane < nv;
+        const float v = ok ? value(rr, c) : 0.0f;
+        if (ok) a.C[rr * a.ldc + n0 + c] = v;
+        const float best = warp_allmax(ok && v == v ? v : kNegInfF);
+        const unsigned hit = __ballot_sync(0xffffffffu, ok && v == best && best > kNegInfF);
+        const int bi = hit ? n0 + sl * 32 + __ffs(hit) - 1 : -1;
+        float mn = ok ? v : __int_as_float(0x7f800000);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if (bi >= 0 && ok) {
+          const float z = __fsub_rn(v, best);
+          e[lane] = __fsub_rn(mn, best) >= -86.5f ? det_expf_nonpos_fast(z) : det_expf_nonpos(z);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          float sum = 0.0f;
+          if (bi >= 0)
+            for (int j = 0; j < nv; ++j) sum = __fadd_rn(sum, e[j]);
+          const long long o = static_cast<long long>(rr) * a.part_ld + (n0 + sl * 32) / 32;
+          a.part_m[o] = best;
+          a.part_s[o] = sum;
+          a.part_arg[o] = bi;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();  // partials reused by the next chunk
+  }
+}
+
+template <int PREC, bool LOGITS>
+void launch_gemv_t(const GemvArgs& a, cudaStream_t st) {
+  constexpr int E = GemvElem<PREC>::bytes;
+  const int row_bytes = a.k_pad * E;
+  if (row_bytes % 128 != 0) fail(kStateError, "gemv: k_pad must be a whole 128-byte slab");
+  if (a.a_mode != 0 && a.K > 32 * kLnKpl) fail(kUsageError, "gemv: LayerNorm rows above 512");
+  const int ksteps = row_bytes / kKStepBytes;
+  // Column groups per chunk (16 columns each) and K ranges: groups x ranges
+  // = 8 warps. Linear layers: one group, K split 8 ways (spreads small
+  // layers over more SMs); projection: whole 32-column slices per chunk.
+  int groups = 1;
+  if (LOGITS) {
+    groups = 2;
+    while (groups < 8 && 16 * (2 * groups) * row_bytes <= 64 * 1024) groups *= 2;
+  }
+  int ks = std::min(kGemvWarps / groups, ksteps);
+  const int chunk = 16 * groups;
+  const int n_chunks = (a.N + chunk - 1) / chunk;
+  const int grid = std::min(148, n_chunks);
+  const int per_cta = (n_chunks + grid - 1) / grid;
+  int nst = std::min(kMaxGemvStages, per_cta);
+  constexpr int kBudget = 227 * 1024;
+  while (nst > 1 && gemv_smem(chunk, ks, row_bytes, nst).total > kBudget) --nst;
+  const GemvSmem L = gemv_smem(chunk, ks, row_bytes, nst);
+  if (L.total > kBudget) fail(kUsageError, "gemv: operand rows too large for shared memory");
+  auto k = gemv_kernel<PREC, LOGITS>;
+  ensure_smem_attr(k, L.total);
+  // Bulk-copy piece size (MTG_GEMV_PIECE bytes, A/B; multiple of 16).
+  static const uint32_t piece = [] {
+    const char* e = std::getenv("MTG_GEMV_PIECE");
+    const long v = e ? std::atol(e) : 1L << 20;  // measured: one copy per chunk is fastest
+    return static_cast<uint32_t>(std::max<long>(16, v / 16 * 16));
+  }();
+  launch_k(k, grid, kGemvThreads, L.total, st, a, chunk, ks, nst, piece);
+  MTG_CUDA(cudaGetLastError());
+}
+
+// One thread per 16-byte lane slot of the fragment-order copy.
+__global__ void gemv_pack_kernel(const uint8_t* __restrict__ w, int n, int row_bytes,
+                                 uint8_t* __restrict__ out, long long slots) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= slots) return;
+  const int lane = static_cast<int>(i & 31);
+  const long long blk = i >> 5;  // (group, K step)
+  const int ksteps = row_bytes / kKStepBytes;
+  const int grp = static_cast<int>(blk / ksteps), st = static_cast<int>(blk % ksteps);
+  const int g = lane >> 2, q = lane & 3;
+  uint32_t v[4];
+#pragma unroll
+  for (int reg = 0; reg < 4; ++reg) {
+    const int row = grp * 16 + g + 8 * (reg & 1);
+    const int off = st * kKStepBytes + 16 * (reg >> 1) + 4 * q;
+    v[reg] = row < n ? *reinterpret_cast<const uint32_t*>(w + static_cast<long long>(row) * row_bytes + off)
+                     : 0u;
+  }
+  *reinterpret_cast<uint4*>(out + i * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+}  // namespace
+
+void launch_gemv_pack(const void* w, int n, int k_pad, int elem, void* out, cudaStream_t st) {
+  const int row_bytes = k_pad * elem;
+  if (row_bytes % 128 != 0) fail(kStateError, "gemv pack: rows must be whole 128-byte slabs");
+  const long long slots = gemv_pack_bytes(n, k_pad, elem) / 16;
+  if (slots == 0) return;
+  gemv_pack_kernel<<<static_cast<unsigned>((slots + 255) / 256), 256, 0, st>>>(
+      static_cast<const uint8_t*>(w), n, row_bytes, static_cast<uint8_t*>(out), slots);
+  MTG_CUDA(cudaGetLastError());
+}
+
+void launch_gemv(int prec, bool logits, const GemvArgs& a, cudaStream_t st) {
+  if (prec == 0)
+    logits ? launch_gemv_t<0, true>(a, st) : launch_gemv_t<0, false>(a, st);
+  else if (prec == 1)
+    logits ? launch_gemv_t<1, true>(a, st) : launch_gemv_t<1, false>(a, st);
+  else
+    logits ? launch_gemv_t<2, true>(a, st) : launch_gemv_t<2, false>(a, st);
+}
+
+}  // namespace mtg

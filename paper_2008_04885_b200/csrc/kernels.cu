@@ -11,6 +11,7 @@
 #include "errors.hpp"
 #include "launch.cuh"
 #include "kernels.cuh"
+#include "rowops.cuh"
 
 namespace mtg {
 
@@ -18,20 +19,11 @@ namespace {
 
 #define kNegInf (-__int_as_float(0x7f800000))
 
-// quant.cpp:113-118
-__device__ __forceinline__ int8_t quant1(float x, float scale) {
-  float v = roundf(__fmul_rn(x, scale));
-  v = fminf(127.0f, fmaxf(-127.0f, v));
-  return static_cast<int8_t>(v);
-}
-__device__ __forceinline__ float qscale_of(float max_abs) {
-  return max_abs == 0.0f ? 1.0f : __fdiv_rn(127.0f, max_abs);
-}
-
 // Writes row r of an operand from x[0..n) with `stride`-spaced workers
 // (a warp: lane/32, a CTA: tid/blockDim). scale is used for int8 only.
 __device__ __forceinline__ void write_operand(const OperandOut& o, long long r, const float* x,
                                               int n, float scale, int tid, int stride) {
+  if (o.prec < 0) return;  // no operand (the consumer converts the fp32 row itself)
   if (o.prec == 0) {
     int8_t* q = o.q + r * o.k_pad;
     for (int c = tid; c < o.k_pad; c += stride) q[c] = c < n ? quant1(x[c], scale) : 0;
@@ -123,39 +115,14 @@ __device__ __forceinline__ void ln_row_regs(float (&xv)[KPL], const float (&gv)[
                                             float* __restrict__ y, long long ldy,
                                             float* __restrict__ rowmax, const OperandOut& op,
                                             int has_op) {
-  float part = 0.0f;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i)
-    if (lane + 32 * i < n) part = __fadd_rn(part, xv[i]);
-  const float nf = static_cast<float>(n);
-  const float mu = __fdiv_rn(warp_allsum(part), nf);
-  float part2 = 0.0f;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i)
-    if (lane + 32 * i < n) {
-      const float dv = __fsub_rn(xv[i], mu);
-      part2 = __fadd_rn(part2, __fmul_rn(dv, dv));
-    }
-  const float var = __fdiv_rn(warp_allsum(part2), nf);
-  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
-  float mx = 0.0f;
   int bad = 0;
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const int c = lane + 32 * i;
-    if (c < n) {
-      xv[i] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[i], mu), inv), gv[i]), bv[i]);
-      mx = fmaxf(mx, fabsf(xv[i]));
-      bad |= !isfinite(xv[i]);
-    }
-  }
+  const float mx = ln_normalize_regs<KPL>(xv, gv, bv, n, lane, &bad);
   if (y) {
     float* yr = y + r * ldy;
 #pragma unroll
     for (int i = 0; i < KPL; ++i)
       if (lane + 32 * i < n) yr[lane + 32 * i] = xv[i];
   }
-  mx = warp_allmax(mx);
   if (rowmax && lane == 0) rowmax[r] = mx;
   if (!has_op) return;
   if (op.prec == 0) {
@@ -323,21 +290,40 @@ __global__ void layernorm_kernel(const float* __restrict__ x, long long ldx, int
   }
   const float var = __fdiv_rn(warp_allsum(part2), nf);
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
-  float* yr = y + r * ldy;
+  // y is optional (decoder LayerNorms only feed the next GEMM): the operand
+  // pass recomputes the normalized values instead of re-reading y.
+  auto norm = [&](int c) {
+    return __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xr[c], mu), inv), g[c]), b[c]);
+  };
   float mx = 0.0f;
   int bad = 0;
   for (int c = lane; c < n; c += 32) {
-    const float v = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xr[c], mu), inv), g[c]), b[c]);
-    yr[c] = v;
+    const float v = norm(c);
+    if (y) y[r * ldy + c] = v;
     mx = fmaxf(mx, fabsf(v));
     bad |= !isfinite(v);
   }
   mx = warp_allmax(mx);
   if (rowmax && lane == 0) rowmax[r] = mx;
-  if (has_op) {
+  if (has_op && op.prec >= 0) {
     if (op.prec == 0 && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(op.nonfinite, 1);
-    __syncwarp();
-    write_operand(op, r, yr, n, qscale_of(mx), lane, 32);
+    const float scale = qscale_of(mx);
+    for (int c = lane; c < op.k_pad; c += 32) {
+      const float v = c < n ? norm(c) : 0.0f;
+      if (op.prec == 0) {
+        op.q[r * op.k_pad + c] = c < n ? quant1(v, scale) : 0;
+      } else if (op.prec == 1) {
+        op.h[r * op.k_pad + c] = __float2bfloat16_rn(v);
+      } else if (op.prec == 3) {
+        op.hi[r * op.k_pad + c] = v;
+      } else {
+        uint32_t hb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+        op.hi[r * op.k_pad + c] = __uint_as_float(hb);
+        op.lo[r * op.k_pad + c] = __fsub_rn(v, __uint_as_float(hb));
+      }
+    }
+    if (op.prec == 0 && lane == 0) op.row_scale[r] = scale;
   }
 }
 
@@ -748,6 +734,10 @@ __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, floa
   __syncwarp();
 }
 
+// Warps per decoder-attention CTA (matches __launch_bounds__(256, 3)); with
+// more heads each warp attends several.
+constexpr int kDecAttnWarps = 8;
+
 // Per-warp smem floats of the decoder attention kernels.
 __host__ __device__ constexpr int dec_attn_warp_floats(int dh, int nkeys) {
   return (dh == 64 ? kStageFloats : 0) + round4(dh) + round4(nkeys);
@@ -770,27 +760,33 @@ __global__ void __launch_bounds__(256, 3)
   if (r >= *d_rows) return;
   const int dh = DH > 0 ? DH : dh_rt;
   const int t = *d_step;
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31, heads = blockDim.x >> 5;
+  // Warp w attends heads w, w + nw, ... (at most 8 warps per CTA).
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int heads = d / dh;
   const int W = dec_attn_warp_floats(DH > 0 ? DH : dh, T);
-  float* stage = sm + h * W;                                 // [kStageFloats] (DH = 64)
+  float* stage = sm + warp * W;                              // [kStageFloats] (DH = 64)
   float* qs = stage + (DH == 64 ? kStageFloats : 0);
   float* ss = qs + round4(dh);
-  float* row = sm + heads * W;                   // [d] context row
+  float* row = sm + nw * W;                      // [d] context row
   float* red = row + d;                          // [33]
   int* arow = reinterpret_cast<int*>(red + 33);  // [T] ancestor rows
   const int* ar = ((t & 1) ? anc1 : anc0) + static_cast<long long>(r) * T;
   for (int j = threadIdx.x; j <= t; j += blockDim.x) arow[j] = ar[j];
-  const long long ld3 = 3LL * d;
-  const float* q = cache + (static_cast<long long>(t) * r_max + r) * ld3 + h * dh;
-  for (int c = lane; c < dh; c += 32) qs[c] = q[c];
   __syncthreads();
-  const float* kb = cache + d + h * dh;
-  auto kp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; };
-  auto vp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d; };
-  if constexpr (DH == 64)
-    attend_warp_staged64(qs, t + 1, scale, kp, vp, stage, ss, row + h * dh);
-  else
-    attend_warp<DH>(qs, t + 1, dh, scale, kp, vp, ss, row + h * dh);
+  const long long ld3 = 3LL * d;
+  for (int h = warp; h < heads; h += nw) {
+    const float* q = cache + (static_cast<long long>(t) * r_max + r) * ld3 + h * dh;
+    for (int c = lane; c < dh; c += 32) qs[c] = q[c];
+    __syncwarp();
+    const float* kb = cache + d + h * dh;
+    auto kp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; };
+    auto vp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d; };
+    if constexpr (DH == 64)
+      attend_warp_staged64(qs, t + 1, scale, kp, vp, stage, ss, row + h * dh);
+    else
+      attend_warp<DH>(qs, t + 1, dh, scale, kp, vp, ss, row + h * dh);
+    __syncwarp();
+  }
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
@@ -809,24 +805,28 @@ __global__ void __launch_bounds__(256, 3)
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
   const int dh = DH > 0 ? DH : dh_rt;
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31, heads = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int heads = d / dh;
   const int s = row_sent[r];
-  const float* kv = ckv + static_cast<long long>(enc_off[s]) * 2 * d + h * dh;
   const int n = enc_len[s];
   const int W = dec_attn_warp_floats(DH > 0 ? DH : dh, max_src);
-  float* stage = sm + h * W;
+  float* stage = sm + warp * W;
   float* qs = stage + (DH == 64 ? kStageFloats : 0);
   float* ss = qs + round4(dh);
-  float* row = sm + heads * W;
+  float* row = sm + nw * W;
   float* red = row + d;
-  for (int c = lane; c < dh; c += 32) qs[c] = cq[r * ldq + h * dh + c];
-  __syncwarp();
-  auto kp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d; };
-  auto vp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; };
-  if constexpr (DH == 64)
-    attend_warp_staged64(qs, n, scale, kp, vp, stage, ss, row + h * dh);
-  else
-    attend_warp<DH>(qs, n, dh, scale, kp, vp, ss, row + h * dh);
+  for (int h = warp; h < heads; h += nw) {
+    const float* kv = ckv + static_cast<long long>(enc_off[s]) * 2 * d + h * dh;
+    for (int c = lane; c < dh; c += 32) qs[c] = cq[r * ldq + h * dh + c];
+    __syncwarp();
+    auto kp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d; };
+    auto vp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; };
+    if constexpr (DH == 64)
+      attend_warp_staged64(qs, n, scale, kp, vp, stage, ss, row + h * dh);
+    else
+      attend_warp<DH>(qs, n, dh, scale, kp, vp, ss, row + h * dh);
+    __syncwarp();
+  }
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
 }
@@ -835,20 +835,39 @@ __global__ void __launch_bounds__(256, 3)
 
 // ---- launchers ------------------------------------------------------------------------------
 
-namespace {
-// Raises a kernel's dynamic shared memory limit (once per size increase).
-void set_smem_limit(const void* fn, size_t bytes, const char* what) {
+void ensure_smem_attr(const void* fn, size_t bytes) {
+  if (bytes > 227 * 1024) fail(kUsageError, "kernel shared memory above 227 KB");
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  MTG_CUDA(cudaGetDevice(&dev));
   static std::mutex mu;
-  static std::map<const void*, size_t> cur;
-  if (bytes > 227 * 1024) fail(kUsageError, std::string(what) + ": shared memory too large");
+  static std::map<std::pair<int, const void*>, size_t> cur;
   std::lock_guard<std::mutex> lock(mu);
-  size_t& c = cur[fn];
-  if (bytes <= 48 * 1024 || bytes <= c) return;
+  size_t& c = cur[{dev, fn}];
+  if (bytes <= c) return;
   MTG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bytes)));
   c = bytes;
 }
+
+namespace {
+void set_smem_limit(const void* fn, size_t bytes, const char* what) {
+  if (bytes > 227 * 1024) fail(kUsageError, std::string(what) + ": shared memory too large");
+  ensure_smem_attr(fn, bytes);
+}
 }  // namespace
+
+namespace {
+__global__ void noop_kernel() {
+  pdl_wait();
+  pdl_trigger();
+}
+}  // namespace
+
+void launch_noop(cudaStream_t st) {
+  launch_k(noop_kernel, 148, 256, 0, st);
+  MTG_CUDA(cudaGetLastError());
+}
 
 void launch_embed_src(const int* ids, const int* pos, int rows, const SrcEmbed& se, int d,
                       float sqrt_d, const float* pe, float* out, long long ldo, cudaStream_t st) {
@@ -967,13 +986,7 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
   if (smem > 227 * 1024)
     fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
   auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
-  static size_t configured[2] = {48 * 1024, 48 * 1024};
-  size_t& cfg = configured[dh == 64 ? 0 : 1];
-  if (smem > cfg) {
-    MTG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    cfg = smem;
-  }
+  ensure_smem_attr(k, smem);
   launch_k(k, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale, ctx,
            ldc, ctx_lo, sent_absmax, nonfinite);
   MTG_CUDA(cudaGetLastError());
@@ -985,11 +998,12 @@ void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const i
                                const OperandOut& op, cudaStream_t st) {
   if (r_max <= 0) return;
   const int dh = d / heads;
-  if (heads > 32) fail(kUsageError, "attention: at most 32 heads");
-  const size_t smem = sizeof(float) * (size_t(heads) * dec_attn_warp_floats(dh, T) + d + 33 + T);
+  if (heads < 1 || heads * dh != d) fail(kUsageError, "attention: heads must divide d_model");
+  const int nw = std::min(heads, kDecAttnWarps);  // warps loop over the heads
+  const size_t smem = sizeof(float) * (size_t(nw) * dec_attn_warp_floats(dh, T) + d + 33 + T);
   auto k = dh == 64 ? dec_self_attention_kernel<64> : dec_self_attention_kernel<0>;
   set_smem_limit(reinterpret_cast<const void*>(k), smem, "decoder self-attention");
-  launch_k(k, r_max, heads * 32, smem, st, qkv_cache, r_max, T, anc0, anc1, d_rows, d_step, d, dh,
+  launch_k(k, r_max, nw * 32, smem, st, qkv_cache, r_max, T, anc0, anc1, d_rows, d_step, d, dh,
            scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
 }
@@ -1001,11 +1015,12 @@ void launch_dec_cross_attention(const float* cq, long long ldq, const float* ckv
                                 cudaStream_t st) {
   if (max_rows <= 0) return;
   const int dh = d / heads;
-  if (heads > 32) fail(kUsageError, "attention: at most 32 heads");
-  const size_t smem = sizeof(float) * (size_t(heads) * dec_attn_warp_floats(dh, max_src) + d + 33);
+  if (heads < 1 || heads * dh != d) fail(kUsageError, "attention: heads must divide d_model");
+  const int nw = std::min(heads, kDecAttnWarps);
+  const size_t smem = sizeof(float) * (size_t(nw) * dec_attn_warp_floats(dh, max_src) + d + 33);
   auto k = dh == 64 ? dec_cross_attention_kernel<64> : dec_cross_attention_kernel<0>;
   set_smem_limit(reinterpret_cast<const void*>(k), smem, "decoder cross-attention");
-  launch_k(k, max_rows, heads * 32, smem, st, cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows,
+  launch_k(k, max_rows, nw * 32, smem, st, cq, ldq, ckv, row_sent, enc_off, enc_len, d_rows,
            max_src, d, dh, scale, ctx, ldc, op);
   MTG_CUDA(cudaGetLastError());
 }

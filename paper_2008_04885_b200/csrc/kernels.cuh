@@ -25,6 +25,9 @@ struct OperandOut {
   int* nonfinite = nullptr;
 };
 
+// Empty dependent kernel (148 CTAs): the PDL launch floor, for timing.
+void launch_noop(cudaStream_t st);
+
 // ---- embeddings (model.cpp:539-581, 624-626) -----------------------------------
 
 // out[r] = table[ids[r]] * sqrt_d + pe[pos[r]]

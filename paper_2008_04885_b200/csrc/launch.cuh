@@ -30,6 +30,30 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// Raises `fn`'s dynamic shared-memory limit to at least `bytes` on the
+// calling thread's current device. Function attributes are per device, so
+// the cache is keyed by (device, function); thread-safe (kernels.cu).
+void ensure_smem_attr(const void* fn, size_t bytes);
+template <typename... KArgs>
+inline void ensure_smem_attr(void (*fn)(KArgs...), size_t bytes) {
+  ensure_smem_attr(reinterpret_cast<const void*>(fn), bytes);
+}
+
+// RAII: makes `device` current for the scope, restoring the previous device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    MTG_CUDA(cudaGetDevice(&prev));
+    if (prev != device) MTG_CUDA(cudaSetDevice(device));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                      cudaStream_t st, Args&&... args) {

@@ -374,15 +374,17 @@ HostModel make_random_model(const ModelConfig& c, uint64_t seed) {
   return m;
 }
 
-// quant.cpp:108-122
+// quantize_model (model.cpp:733-748) + quantize (quant.cpp:108-122): every
+// parameter is checked for non-finite values in name order (check_finite runs
+// before the quantizable test), then the quantizable ones get one scale each.
 void quantize_weights(HostModel& m) {
   for (auto& [name, t] : m.params) {
-    if (!is_quantized_param(name) || t.is_int8) continue;
-    float max_abs = 0.0f;
-    for (float v : t.f32) {
+    if (t.is_int8) continue;
+    for (float v : t.f32)
       if (!std::isfinite(v)) fail(kValueError, "quantize_model(" + name + "): non-finite values");
-      max_abs = std::max(max_abs, std::fabs(v));
-    }
+    if (!is_quantized_param(name)) continue;
+    float max_abs = 0.0f;
+    for (float v : t.f32) max_abs = std::max(max_abs, std::fabs(v));
     t.scale = max_abs == 0.0f ? 1.0f : 127.0f / max_abs;
     t.q.resize(t.f32.size());
     for (size_t i = 0; i < t.f32.size(); ++i) {

@@ -471,17 +471,7 @@ void launch_topk_select(const float* logits, long long ldl, const float* part_m,
   TailArgs ta{logits, ldl, part_m, part_s, part_arg, part_ld, nsub};
   const ShortlistArgs none{};
   auto launch = [&](auto kern) {
-    static std::mutex mu;
-    static std::map<const void*, size_t> configured;  // per kernel instantiation
-    {
-      std::lock_guard<std::mutex> lock(mu);
-      size_t& c = configured[reinterpret_cast<const void*>(kern)];
-      if (smem > 48 * 1024 && smem > c) {
-        MTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        c = smem;
-      }
-    }
+    ensure_smem_attr(kern, smem);
     launch_k(kern, b.N, kMT * G, smem, st, ta, sa ? *sa : none, b);
   };
   if (!sa) launch(topk_select_kernel<0>);

@@ -71,6 +71,15 @@ int main(int argc, char** argv) {
   }
   CHECK(beam.tokens == greedy);
 
+  // decode.cpp:48 with max_len <= 0: no search step, the source is still
+  // encoded (bad ids throw), the unfinished root comes back truncated.
+  BeamConfig none;
+  none.max_len = 0;
+  Hypothesis root = beam_search(micro, src, {}, none);
+  CHECK(root.tokens.empty() && root.logprob == 0.0f && root.truncated && !root.finished);
+  CHECK(root.normalized == 0.0f);
+  CHECK(throws<IndexError>([&] { beam_search(micro, {4, 99, kEosId}, {}, none); }));
+
   // test_decode.cpp:171-206 latency percentiles from an injected clock on the
   // all-zero model: 10 sentences, sentence i takes (i+1) ms.
   GpuExecutor zero(argv[1], MTG_PREC_F32);
