@@ -69,6 +69,12 @@ struct AttnSmallArgs {
   const int* anc1;
   const int* row_parent;
   int reorder;
+  // history reorder (beam.cu beam_reorder_kernel), done by the layer-0
+  // attention: row r's ancestry / token tables of step t
+  int hist;
+  int* anc_out[2];
+  int* tok_out[2];
+  const int* row_prev;
   // cross
   const float* cq;
   long long ldq;
@@ -76,6 +82,7 @@ struct AttnSmallArgs {
   const int* row_sent;
   const int* enc_off;
   const int* enc_len;
+  KTrace trace;
 };
 
 __global__ void __launch_bounds__(kAttnThreads)
@@ -104,6 +111,17 @@ __global__ void __launch_bounds__(kAttnThreads)
       for (int j = tid; j < t; j += blockDim.x) arow[j] = src[j];
       if (tid == 0) arow[t] = r;
       __syncthreads();
+      if (a.hist && a.reorder && t >= 1 && h == 0) {
+        // Nothing reads step t's tables before this kernel (the attention
+        // derives the ancestry from the parent): the next step's attention
+        // and this step's beam selection come later.
+        int* an = a.anc_out[t & 1] + static_cast<long long>(r) * a.T;
+        const int* tc = a.tok_out[(t - 1) & 1] + static_cast<long long>(a.row_parent[r]) * a.T;
+        int* tn = a.tok_out[t & 1] + static_cast<long long>(r) * a.T;
+        for (int j = tid; j <= t && j < a.T; j += blockDim.x) an[j] = arow[j];
+        for (int j = tid; j < t - 1; j += blockDim.x) tn[j] = tc[j];
+        if (tid == 0 && t - 1 < a.T) tn[t - 1] = a.row_prev[r];
+      }
       const long long ld3 = 3LL * d;
       const float* kb = a.cache + d + h * kDh;
       stage_kv(
@@ -123,7 +141,11 @@ __global__ void __launch_bounds__(kAttnThreads)
   }
   pdl_wait();
   pdl_trigger();
-  if (r >= R) return;
+  trace_begin(a.trace);
+  if (r >= R) {
+    trace_end(a.trace);
+    return;
+  }
   float* V = K + Tk * kDh;
   float* q = V + Tk * kDh;  // [64]
   float* s = q + 2 * kDh;   // [n] scores -> probabilities
@@ -180,6 +202,7 @@ __global__ void __launch_bounds__(kAttnThreads)
     for (int j = 0; j < n; ++j) acc = __fadd_rn(acc, __fmul_rn(s[j], V[swz(j, c4) + e]));
     a.ctx[r * a.ldc + h * kDh + c] = acc;
   }
+  trace_end(a.trace);
 }
 
 size_t attn_small_smem(int keys) {
@@ -193,11 +216,19 @@ bool attn_small_supported(int d, int heads, int T, int max_src) {
   return heads > 0 && d == heads * kDh && attn_small_smem(std::max(T, max_src)) <= 200 * 1024;
 }
 
-void launch_attn_small_self(const float* cache, int r_max, int T, const int* anc0,
-                            const int* anc1, const int* row_parent, int reorder,
-                            const int* d_rows, const int* d_step, int rows_alloc, int d,
-                            int heads, float scale, float* ctx, long long ldc, cudaStream_t st) {
+void launch_attn_small_self(const float* cache, int r_max, int T, int* anc0, int* anc1,
+                            const int* row_parent, int reorder, int* tok0, int* tok1,
+                            const int* row_prev, int hist, const int* d_rows, const int* d_step,
+                            int rows_alloc, int d, int heads, float scale, float* ctx,
+                            long long ldc, cudaStream_t st, const KTrace& tr) {
   AttnSmallArgs a{};
+  a.hist = hist;
+  a.anc_out[0] = anc0;
+  a.anc_out[1] = anc1;
+  a.tok_out[0] = tok0;
+  a.tok_out[1] = tok1;
+  a.row_prev = row_prev;
+  a.trace = tr;
   a.self_mode = 1;
   a.d_rows = d_rows;
   a.d_step = d_step;
@@ -222,8 +253,10 @@ void launch_attn_small_self(const float* cache, int r_max, int T, const int* anc
 void launch_attn_small_cross(const float* cq, long long ldq, const float* ckv,
                              const int* row_sent, const int* enc_off, const int* enc_len,
                              const int* d_rows, int rows_alloc, int max_src, int d, int heads,
-                             float scale, float* ctx, long long ldc, cudaStream_t st) {
+                             float scale, float* ctx, long long ldc, cudaStream_t st,
+                             const KTrace& tr) {
   AttnSmallArgs a{};
+  a.trace = tr;
   a.self_mode = 0;
   a.d_rows = d_rows;
   a.rows_alloc = rows_alloc;

@@ -55,10 +55,12 @@ __global__ void __launch_bounds__(kSelWarps * 32) beam_select_kernel(BeamDev b) 
   int* row0_s = sel_smem + b.N;
   __shared__ int is_last;
   const int t = *b.step;
+  trace_begin_at(b.tr_b, t);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int s = blockIdx.x * nwarps + warp; s < b.N; s += gridDim.x * nwarps)
     select_sentence(b, s, t, lane);
   finish_select(b, t, live_s, row0_s, &is_last);
+  trace_end_at(b.tr_b, t);
 }
 
 __global__ void beam_reorder_kernel(BeamDev b) {

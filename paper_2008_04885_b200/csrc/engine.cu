@@ -224,6 +224,7 @@ Engine::Engine(HostModel model, int precision, int device)
     fail(kUsageError, "unknown precision " + std::to_string(prec_));
   if (host_.quantized && prec_ != kINT8) prec_ = kINT8;  // tools/minimt.cpp:317-320
   if (const char* e = std::getenv("MTG_DIAG_EVENTS")) diag_ = e[0] == '1';
+  if (const char* e = std::getenv("MTG_TRACE")) trace_ = e[0] == '1';
   if (const char* e = std::getenv("MTG_NO_SPLIT_K")) split_k_ = e[0] != '1';
   if (prec_ == kINT8 && !host_.quantized) quantize_weights(host_);
   const ModelConfig& c = host_.config;
@@ -396,6 +397,11 @@ void Engine::ensure_workspace(int n_sent, int m_enc, int beam) {
   src_pos_.resize(M);
   src_off_.resize(N + 1);
   sent_absmax_.resize(N);
+  if (gemv_ws_.size() == 0) {  // split-K partials and tickets of the GEMV kernels
+    gemv_ws_.resize(size_t(1) << 18);
+    gemv_sem_.resize(4096);
+    MTG_CUDA(cudaMemsetAsync(gemv_sem_.get(), 0, gemv_sem_.size() * sizeof(int), stream_));
+  }
   enc_off_.resize(N);
   enc_len_.resize(N);
   nonfinite_.resize(1);
@@ -565,7 +571,8 @@ void Engine::diag_clear() {
   enc_runs_ = 0;
 }
 
-std::string Engine::diag_report() const {
+std::string Engine::diag_report() {
+  if (trace_) return trace_report();
   std::string out = "steps " + std::to_string(diag_steps_) + "\n";
   if (diag_steps_ == 0) return out;
   double total = 0.0;
@@ -980,6 +987,77 @@ GemvArgs Engine::gemv_args(const DevLinear& w) const {
   return g;
 }
 
+KTrace Engine::next_trace(const char* name) {
+  KTrace k;
+  if (!trace_) return k;
+  const int per = 8 * host_.config.num_decoder_layers + 3;
+  if (trace_buf_.size() < size_t(2) * T_ * per) return k;  // sized by trace_reset
+  if (static_cast<int>(trace_names_.size()) <= trace_slot_) trace_names_.push_back(name);
+  k.buf = trace_buf_.get();
+  k.slot = trace_slot_++;
+  k.per_step = per;
+  k.d_step = step_.get();
+  trace_per_step_ = per;
+  return k;
+}
+
+void Engine::trace_reset() {
+  if (!trace_) return;
+  const size_t need = size_t(2) * T_ * (8 * host_.config.num_decoder_layers + 3);
+  if (trace_buf_.size() < need) trace_buf_.resize(need);
+  std::vector<unsigned long long> init(trace_buf_.size());
+  for (size_t i = 0; i < init.size(); ++i) init[i] = (i & 1) ? 0ull : ~0ull;
+  trace_buf_.upload(init.data(), init.size(), stream_);
+}
+
+// Per kernel of the step: mean gap from the previous traced kernel's last CTA
+// exit to this kernel's first post-wait CTA, and mean duration (post-wait to
+// last exit); "tail" = from the last traced kernel of a step to the first of
+// the next (top-k + beam select + launch gaps).
+std::string Engine::trace_report() {
+  if (!trace_ || trace_per_step_ == 0) return "";
+  std::vector<unsigned long long> b(trace_buf_.size());
+  MTG_CUDA(cudaStreamSynchronize(stream_));
+  trace_buf_.download(b.data(), b.size());
+  const int per = trace_per_step_;
+  // slots that recorded anything (a fused tail leaves one unused)
+  std::vector<int> used;
+  for (int k = 0; k < per; ++k)
+    if (b[2 * k] != ~0ull) used.push_back(k);
+  std::vector<double> gap(per, 0.0), dur(per, 0.0);
+  double total = 0.0;
+  int steps = 0;
+  for (int t = 0; t + 1 < T_; ++t) {
+    const unsigned long long* s = b.data() + size_t(2) * t * per;
+    const unsigned long long* nx = s + 2 * per;
+    bool ok = nx[2 * used[0]] != ~0ull;
+    for (int k : used) ok = ok && s[2 * k] != ~0ull && s[2 * k + 1] != 0ull;
+    if (!ok) break;
+    ++steps;
+    for (size_t u = 0; u < used.size(); ++u) {
+      const int k = used[u];
+      dur[k] += double(s[2 * k + 1]) - double(s[2 * k]);
+      if (u > 0) gap[k] += double(s[2 * k]) - double(s[2 * used[u - 1] + 1]);
+    }
+    gap[used[0]] += double(nx[2 * used[0]]) - double(s[2 * used.back() + 1]);
+    total += double(nx[2 * used[0]]) - double(s[2 * used[0]]);
+  }
+  if (steps == 0) return "trace: no complete step\n";
+  std::string out = "trace (" + std::to_string(steps) + " steps, us): gap before / duration\n";
+  for (int k : used) {
+    char line[200];
+    std::snprintf(line, sizeof line, "  %2d %-34s %6.2f  %6.2f\n", k,
+                  k < static_cast<int>(trace_names_.size()) ? trace_names_[k].c_str() : "?",
+                  gap[k] / steps / 1000.0, dur[k] / steps / 1000.0);
+    out += line;
+  }
+  char tl[200];
+  std::snprintf(tl, sizeof tl, "  step %.2f us (first kernel's gap: from the previous step's last)\n",
+                total / steps / 1000.0);
+  out += tl;
+  return out;
+}
+
 // decode_step (model.cpp:614-672) for <= kGemvRows live rows: per decoder
 // layer QKV, self-attention, Wo(+res), cross-Wq, cross-attention,
 // cross-Wo(+res), W1(+b1, ReLU), W2(+b2, res); the LayerNorms, the target
@@ -993,6 +1071,7 @@ void Engine::decoder_body_small(bool reorder) {
   const float sqrt_d = std::sqrt(static_cast<float>(c.d_model));
   const float scale = 1.0f / std::sqrt(static_cast<float>(d_ / heads_));
   const int gp = prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2;
+  trace_slot_ = 0;
   OperandOut none;
   none.prec = -1;  // attention writes the fp32 context only
   static const bool small_attn_env = [] {
@@ -1009,7 +1088,8 @@ void Engine::decoder_body_small(bool reorder) {
     g.sqrt_d = sqrt_d;
     g.x_out = dec_y_.get();
     g.ldx_out = d;
-    g.reorder = reorder ? 1 : 0;
+    // with the small attention, the layer-0 attention kernel does the reorder
+    g.reorder = reorder && !(small_attn && c.num_decoder_layers > 0) ? 1 : 0;
     g.row_parent = row_parent_.get();
     g.anc[0] = anc0_.get();
     g.anc[1] = anc1_.get();
@@ -1048,12 +1128,15 @@ void Engine::decoder_body_small(bool reorder) {
     q.ln_b = L.n1.b.get();
     out_to(q, qkv_cache_[l].get(), 3 * d, nullptr, false, 0);
     q.c_step_stride = static_cast<long long>(R) * 3 * d;
+    q.trace = next_trace(l == 0 ? "gemv qkv (+embed, LN)" : "gemv qkv (+LN)");
     launch_gemv(gp, false, q, stream_);
     count(l == 0 ? "gemv qkv (+embed, LN)" : "gemv qkv (+LN)");
     if (small_attn) {
       launch_attn_small_self(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(),
-                             row_parent_.get(), reorder ? 1 : 0, dr, step_.get(),
-                             std::min(R, kGemvRows), d_, heads_, scale, dec_ctx_.get(), d, stream_);
+                             row_parent_.get(), reorder ? 1 : 0, tok0_.get(), tok1_.get(),
+                             row_prev_.get(), l == 0 ? 1 : 0, dr, step_.get(),
+                             std::min(R, kGemvRows), d_, heads_, scale, dec_ctx_.get(), d, stream_,
+                             next_trace("self attention"));
     } else {
       launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
                                 step_.get(), d_, heads_, scale, dec_ctx_.get(), d, none, stream_);
@@ -1062,17 +1145,19 @@ void Engine::decoder_body_small(bool reorder) {
     GemvArgs o = gemv_args(L.self_wo);
     rows_from(o, dec_ctx_.get(), d);
     out_to(o, dec_y_.get(), d, nullptr, true, 0);
+    o.trace = next_trace("gemv wo (+res)");
     launch_gemv(gp, false, o, stream_);
     count("gemv wo (+res)");
     GemvArgs cq = gemv_args(L.cross_q);
     ln_from(cq, L.n2);
     out_to(cq, dec_cq_.get(), d, nullptr, false, 0);
+    cq.trace = next_trace("gemv cross wq (+LN)");
     launch_gemv(gp, false, cq, stream_);
     count("gemv cross wq (+LN)");
     if (small_attn) {
       launch_attn_small_cross(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
                               enc_len_.get(), dr, std::min(R, kGemvRows), T_, d_, heads_, scale,
-                              dec_ctx_.get(), d, stream_);
+                              dec_ctx_.get(), d, stream_, next_trace("cross attention"));
     } else {
       launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
                                  enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d,
@@ -1082,16 +1167,32 @@ void Engine::decoder_body_small(bool reorder) {
     GemvArgs co = gemv_args(L.cross_wo);
     rows_from(co, dec_ctx_.get(), d);
     out_to(co, dec_y_.get(), d, nullptr, true, 0);
+    co.trace = next_trace("gemv cross wo (+res)");
     launch_gemv(gp, false, co, stream_);
     count("gemv cross wo (+res)");
     GemvArgs f1 = gemv_args(L.w1);
     ln_from(f1, L.n3);
     out_to(f1, ffh_.get(), dff_, L.b1.get(), false, 1);
+    f1.trace = next_trace("gemv w1 (+LN, b1, relu)");
     launch_gemv(gp, false, f1, stream_);
     count("gemv w1 (+LN, b1, relu)");
     GemvArgs f2 = gemv_args(L.w2);
     rows_from(f2, ffh_.get(), dff_);
     out_to(f2, dec_y_.get(), d, L.b2.get(), true, 0);
+    // fp32 / bf16 FFN-down with a long K: split K over 4 CTAs per column
+    // chunk (more SMs stream the weights; partials added in split order).
+    // int8 rows need their whole-row max, so they stay unsplit.
+    static const int w2_split = [] {
+      const char* e = std::getenv("MTG_GEMV_W2_SPLIT");
+      return e ? std::atoi(e) : 4;
+    }();
+    if (prec_ != kINT8 && w2_split > 1 && L.w2.k_pad * (prec_ == kF32 ? 4 : 2) % (w2_split * 128) == 0 &&
+        L.w2.k_pad >= 1024) {
+      f2.ksplit = w2_split;
+      f2.ws = gemv_ws_.get();
+      f2.sem = gemv_sem_.get();
+    }
+    f2.trace = next_trace("gemv w2 (+b2, res)");
     launch_gemv(gp, false, f2, stream_);
     count("gemv w2 (+b2, res)");
   }
@@ -1108,6 +1209,7 @@ void Engine::decoder_body_small(bool reorder) {
   lg.part_s = part_s_.get();
   lg.part_arg = part_arg_.get();
   lg.part_ld = part_ld_;
+  lg.trace = next_trace("gemv logits + partials (+LN)");
   launch_gemv(gp, true, lg, stream_);
   count("gemv logits + softmax partials (+LN)");
 }
@@ -1341,24 +1443,33 @@ void Engine::capture_one_step() {
     }();
     const int sl_prec = prec_ == kINT8 ? 0 : prec_ == kBF16 ? 1 : 2;
     const ShortlistArgs sla = shortlist_args();
+    BeamDev bd = beam_;  // + trace slots of the step tail (MTG_TRACE)
     static const int fused_min_n = [] {  // measured: neutral-to-worse for batch-1
       const char* e = std::getenv("MTG_FUSED_TAIL_MIN_N");
       return e ? std::atoi(e) : 8;
     }();
     if (fused_tail && beam_.N >= fused_min_n) {
+      if (small_path()) {
+        bd.tr_a = next_trace("fused top-k + select");
+        next_trace("(unused)");
+      }
       launch_topk_select(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
-                         part_ld_, use_shortlist_ ? &sla : nullptr, sl_prec, beam_, stream_);
+                         part_ld_, use_shortlist_ ? &sla : nullptr, sl_prec, bd, stream_);
       count("top-k + beam select");
     } else {
+      if (small_path()) {
+        bd.tr_a = next_trace("softmax + top-k");
+        bd.tr_b = next_trace("beam select");
+      }
       if (use_shortlist_) {
-        launch_shortlist_topk(sl_prec, sla, beam_, stream_);
+        launch_shortlist_topk(sl_prec, sla, bd, stream_);
         count("shortlist logits + softmax + top-k");
       } else {
         launch_softmax_topk(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
-                            part_ld_, beam_, stream_);
+                            part_ld_, bd, stream_);
         count("softmax + top-k merge");
       }
-      launch_beam_select(beam_, stream_);
+      launch_beam_select(bd, stream_);
       count("beam select");
     }
   }
@@ -1565,6 +1676,7 @@ void Engine::run_staged(const BeamConfigC& cfg) {
   beam_.N = n;
   beam_.B = cfg.beam_size;
   beam_.alpha = cfg.alpha;
+  trace_reset();
   run_encoder(n, staged_m_, staged_max_src_);
   if (t_run > 0) decode_loop(t_run);
   last_launches_ = launches_;
@@ -1695,7 +1807,8 @@ void Engine::time_kernel(int kernel, int iters, float* ms, double* bytes, double
     } else if (kernel == 16) {  // small-batch self-attention (attn_small.cu)
       one = [&, scale] {
         launch_attn_small_self(qkv_cache_[0].get(), r_max_, T_, anc0_.get(), anc1_.get(),
-                               row_parent_.get(), 1, n_rows_.get(), step_.get(),
+                               row_parent_.get(), 1, tok0_.get(), tok1_.get(), row_prev_.get(), 0,
+                               n_rows_.get(), step_.get(),
                                std::min(r_max_, kGemvRows), d_, heads_, scale, dec_ctx_.get(), d_,
                                stream_);
       };

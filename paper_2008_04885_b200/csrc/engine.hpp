@@ -98,7 +98,7 @@ class Engine {
              const std::vector<std::vector<int>>* shortlists = nullptr);
   void run_staged(const BeamConfigC& cfg);
   int64_t last_launches() const { return last_launches_; }
-  std::string diag_report() const;  // per-kernel step times (MTG_DIAG_EVENTS=1)
+  std::string diag_report();  // per-kernel step times (MTG_DIAG_EVENTS=1)
   cudaStream_t stream() const { return stream_; }
   // Times one hot kernel in isolation on the staged batch (see minimt_gpu.h).
   void time_kernel(int kernel, int iters, float* ms, double* bytes, double* flops);
@@ -129,6 +129,16 @@ class Engine {
   bool small_path() const;
   void decoder_body_small(bool reorder);
   GemvArgs gemv_args(const DevLinear& w) const;
+  DeviceBuffer<float> gemv_ws_;       // split-K partials
+  DeviceBuffer<int> gemv_sem_;        // split-K tickets (zero between launches)
+  // MTG_TRACE=1: in-graph timeline of the small-batch step kernels.
+  bool trace_ = false;
+  DeviceBuffer<unsigned long long> trace_buf_;
+  int trace_slot_ = 0, trace_per_step_ = 0;
+  std::vector<std::string> trace_names_;
+  KTrace next_trace(const char* name);
+  void trace_reset();
+  std::string trace_report();
   void decode_loop(int t_run);
   // Launch accounting; with MTG_DIAG_EVENTS=1 the step graph also records an
   // event after every kernel (breaks PDL overlap -- diagnostics only) and

@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
+
 namespace mtg {
 
 constexpr int kGemvRows = 8;
@@ -72,6 +74,13 @@ struct GemvArgs {
   int* part_arg = nullptr;
   long long part_ld = 0;
   int* nonfinite = nullptr;
+  // ---- split-K across CTAs (fp32 / bf16 plain operand rows): partials in
+  // ws, the last CTA of a chunk (ticket in sem, one int per chunk,
+  // zero-initialised) adds them in split order ----
+  int ksplit = 1;
+  float* ws = nullptr;
+  int* sem = nullptr;
+  KTrace trace;
 };
 
 // prec: 0 int8, 1 bf16, 2 fp32. logits: output-projection epilogue.
@@ -93,13 +102,17 @@ void launch_gemv_pack(const void* w, int n, int k_pad, int elem, void* out, cuda
 // dim 64, keys / values prefetched before the programmatic-dependency wait;
 // fp32 contexts only (the consuming GEMV builds the operand).
 bool attn_small_supported(int d, int heads, int T, int max_src);
-void launch_attn_small_self(const float* cache, int r_max, int T, const int* anc0,
-                            const int* anc1, const int* row_parent, int reorder,
-                            const int* d_rows, const int* d_step, int rows_alloc, int d,
-                            int heads, float scale, float* ctx, long long ldc, cudaStream_t st);
+// hist != 0 (layer 0 of a beam step): also writes the step's ancestry /
+// token-history rows (the beam reorder), off the step's critical path.
+void launch_attn_small_self(const float* cache, int r_max, int T, int* anc0, int* anc1,
+                            const int* row_parent, int reorder, int* tok0, int* tok1,
+                            const int* row_prev, int hist, const int* d_rows, const int* d_step,
+                            int rows_alloc, int d, int heads, float scale, float* ctx,
+                            long long ldc, cudaStream_t st, const KTrace& tr = {});
 void launch_attn_small_cross(const float* cq, long long ldq, const float* ckv,
                              const int* row_sent, const int* enc_off, const int* enc_len,
                              const int* d_rows, int rows_alloc, int max_src, int d, int heads,
-                             float scale, float* ctx, long long ldc, cudaStream_t st);
+                             float scale, float* ctx, long long ldc, cudaStream_t st,
+                             const KTrace& tr = {});
 
 }  // namespace mtg

@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
+
 namespace mtg {
 
 constexpr int kMaxBeam = 16;
@@ -166,6 +168,7 @@ struct BeamDev {
   int N, B, T, R_max, V;
   float alpha;
   int max_seq_len;
+  KTrace tr_a, tr_b;  // MTG_TRACE: top-k (or fused tail) and beam select
 };
 
 // Step 0: one root row (BOS, logprob 0) per active sentence.

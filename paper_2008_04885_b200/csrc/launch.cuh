@@ -22,6 +22,38 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// In-graph kernel timeline (MTG_TRACE=1, diagnostics only): a traced kernel
+// records the first post-wait time of its CTAs and the last CTA exit time
+// (%globaltimer, ns) into buf[2 * (step * per_step + slot) + {0, 1}].
+struct KTrace {
+  unsigned long long* buf = nullptr;
+  int slot = 0;
+  int per_step = 0;
+  const int* d_step = nullptr;
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_begin(const KTrace& k) {
+  if (k.buf && threadIdx.x == 0)
+    atomicMin(&k.buf[2 * (static_cast<long long>(*k.d_step) * k.per_step + k.slot)], gtimer());
+}
+__device__ __forceinline__ void trace_end(const KTrace& k) {
+  if (k.buf && threadIdx.x == 0)
+    atomicMax(&k.buf[2 * (static_cast<long long>(*k.d_step) * k.per_step + k.slot) + 1], gtimer());
+}
+// Variants with the step passed in (kernels that advance the step counter).
+__device__ __forceinline__ void trace_begin_at(const KTrace& k, int t) {
+  if (k.buf && threadIdx.x == 0)
+    atomicMin(&k.buf[2 * (static_cast<long long>(t) * k.per_step + k.slot)], gtimer());
+}
+__device__ __forceinline__ void trace_end_at(const KTrace& k, int t) {
+  if (k.buf && threadIdx.x == 0)
+    atomicMax(&k.buf[2 * (static_cast<long long>(t) * k.per_step + k.slot) + 1], gtimer());
+}
+
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("MTG_NO_PDL");

@@ -249,10 +249,13 @@ __global__ void __launch_bounds__(kMT)
                         BeamDev b) {
   pdl_wait();
   pdl_trigger();
+  const int t0 = b.tr_a.buf ? *b.step : 0;
+  trace_begin_at(b.tr_a, t0);
   __shared__ MergeScratch sc;
   const int r = blockIdx.x;
-  if (r >= *b.n_rows) return;  // uniform over the CTA
-  merge_row(r, logits, ldl, part_m, part_s, part_arg, part_ld, nsub, b, threadIdx.x, 0, sc);
+  if (r < *b.n_rows)  // uniform over the CTA
+    merge_row(r, logits, ldl, part_m, part_s, part_arg, part_ld, nsub, b, threadIdx.x, 0, sc);
+  trace_end_at(b.tr_a, t0);
 }
 
 // ---- vocabulary shortlist (decode.cpp:55-61 with rows; model.cpp:440-449) ----
@@ -433,6 +436,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   __shared__ int is_last;
   const int s = blockIdx.x;
   const int t = *b.step;
+  trace_begin_at(b.tr_a, t);
   if (!b.sent_done[s]) {
     const int L = b.sent_live[s], r0 = b.sent_row0[s];
     for (int i = g; i < L; i += G) {
@@ -446,6 +450,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   __syncthreads();
   if (threadIdx.x < 32) select_sentence(b, s, t, threadIdx.x);
   finish_select(b, t, live_s, row0_s, &is_last);
+  trace_end_at(b.tr_a, t);
 }
 
 }  // namespace
