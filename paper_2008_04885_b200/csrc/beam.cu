@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) beam_select_kernel(BeamDev b) 
 __global__ void beam_reorder_kernel(BeamDev b) {
   pdl_wait();
   pdl_trigger();
+  trace_begin(b.tr_b);  // (the fused step tail leaves tr_b to the reorder)
   const int r = blockIdx.x;
   if (r >= *b.n_rows) return;
   const int tn = *b.step;
@@ -83,6 +84,7 @@ __global__ void beam_reorder_kernel(BeamDev b) {
     if (tn < T) an[tn] = r;
     if (tn - 1 < T) tnw[tn - 1] = b.row_prev[r];
   }
+  trace_end(b.tr_b);
 }
 
 }  // namespace

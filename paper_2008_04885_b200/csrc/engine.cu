@@ -531,6 +531,8 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   ep.d_M = d_m;
   ep.N = w.n;
   ep.C_lo = c_lo;
+  ep.tr = cur_tr_;
+  cur_tr_ = KTrace{};
   if (seg_absmax) {
     if (residual) fail(kStateError, "gemm: sentence-max epilogue takes no residual");
     ep.seg_absmax = seg_absmax;
@@ -678,6 +680,8 @@ void Engine::gemm_logits(int m, const int* d_m) {
   ep.part_s = part_s_.get();
   ep.part_arg = part_arg_.get();
   ep.part_ld = part_ld_;
+  ep.tr = cur_tr_;
+  cur_tr_ = KTrace{};
   launch_gemm(it->second, ep, stream_);
   count("logits gemm + softmax partials");
 }
@@ -990,8 +994,9 @@ GemvArgs Engine::gemv_args(const DevLinear& w) const {
 KTrace Engine::next_trace(const char* name) {
   KTrace k;
   if (!trace_) return k;
-  const int per = 8 * host_.config.num_decoder_layers + 3;
+  const int per = kTraceSlots;
   if (trace_buf_.size() < size_t(2) * T_ * per) return k;  // sized by trace_reset
+  if (trace_slot_ >= per) return k;
   if (static_cast<int>(trace_names_.size()) <= trace_slot_) trace_names_.push_back(name);
   k.buf = trace_buf_.get();
   k.slot = trace_slot_++;
@@ -1003,7 +1008,7 @@ KTrace Engine::next_trace(const char* name) {
 
 void Engine::trace_reset() {
   if (!trace_) return;
-  const size_t need = size_t(2) * T_ * (8 * host_.config.num_decoder_layers + 3);
+  const size_t need = size_t(2) * T_ * kTraceSlots;
   if (trace_buf_.size() < need) trace_buf_.resize(need);
   std::vector<unsigned long long> init(trace_buf_.size());
   for (size_t i = 0; i < init.size(); ++i) init[i] = (i & 1) ? 0ull : ~0ull;
@@ -1020,35 +1025,42 @@ std::string Engine::trace_report() {
   MTG_CUDA(cudaStreamSynchronize(stream_));
   trace_buf_.download(b.data(), b.size());
   const int per = trace_per_step_;
-  // slots that recorded anything (a fused tail leaves one unused)
-  std::vector<int> used;
-  for (int k = 0; k < per; ++k)
-    if (b[2 * k] != ~0ull) used.push_back(k);
+  auto valid = [&](const unsigned long long* s, int k) { return s[2 * k] != ~0ull && s[2 * k + 1] != 0ull; };
   std::vector<double> gap(per, 0.0), dur(per, 0.0);
+  std::vector<int> ngap(per, 0), ndur(per, 0);
   double total = 0.0;
   int steps = 0;
   for (int t = 0; t + 1 < T_; ++t) {
     const unsigned long long* s = b.data() + size_t(2) * t * per;
     const unsigned long long* nx = s + 2 * per;
-    bool ok = nx[2 * used[0]] != ~0ull;
-    for (int k : used) ok = ok && s[2 * k] != ~0ull && s[2 * k + 1] != 0ull;
-    if (!ok) break;
-    ++steps;
-    for (size_t u = 0; u < used.size(); ++u) {
-      const int k = used[u];
+    int first = -1, prev = -1, last = -1, nfirst = -1;
+    for (int k = 0; k < per; ++k) {
+      if (!valid(s, k)) continue;
+      if (first < 0) first = k;
       dur[k] += double(s[2 * k + 1]) - double(s[2 * k]);
-      if (u > 0) gap[k] += double(s[2 * k]) - double(s[2 * used[u - 1] + 1]);
+      ++ndur[k];
+      if (prev >= 0) {
+        gap[k] += double(s[2 * k]) - double(s[2 * prev + 1]);
+        ++ngap[k];
+      }
+      prev = last = k;
     }
-    gap[used[0]] += double(nx[2 * used[0]]) - double(s[2 * used.back() + 1]);
-    total += double(nx[2 * used[0]]) - double(s[2 * used[0]]);
+    for (int k = 0; k < per && nfirst < 0; ++k)
+      if (valid(nx, k)) nfirst = k;
+    if (first < 0 || nfirst < 0) break;
+    gap[nfirst] += double(nx[2 * nfirst]) - double(s[2 * last + 1]);
+    ++ngap[nfirst];
+    total += double(nx[2 * nfirst]) - double(s[2 * first]);
+    ++steps;
   }
   if (steps == 0) return "trace: no complete step\n";
   std::string out = "trace (" + std::to_string(steps) + " steps, us): gap before / duration\n";
-  for (int k : used) {
+  for (int k = 0; k < per; ++k) {
+    if (ndur[k] == 0) continue;
     char line[200];
     std::snprintf(line, sizeof line, "  %2d %-34s %6.2f  %6.2f\n", k,
                   k < static_cast<int>(trace_names_.size()) ? trace_names_[k].c_str() : "?",
-                  gap[k] / steps / 1000.0, dur[k] / steps / 1000.0);
+                  ngap[k] ? gap[k] / ngap[k] / 1000.0 : 0.0, dur[k] / ndur[k] / 1000.0);
     out += line;
   }
   char tl[200];
@@ -1229,8 +1241,15 @@ void Engine::decoder_body(bool reorder) {
   // Executor::linear call in decode_step), so LayerNorm and attention write
   // the next GEMM's operand directly.
   const OperandOut od = opout(act_d_);
+  trace_slot_ = 0;
+  auto tr_od = [&](const char* name) {  // operand writer with a timeline slot (MTG_TRACE)
+    OperandOut o = od;
+    o.tr = next_trace(name);
+    return o;
+  };
   auto ln_dec = [&](const LN& ln, float* y = nullptr) {
-    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), y, d, nullptr, &od,
+    const OperandOut o = tr_od("layernorm");
+    launch_layernorm(dec_y_.get(), d, R, dr, d_, ln.g.get(), ln.b.get(), y, d, nullptr, &o,
                      stream_);
     count("layernorm");
   };
@@ -1274,7 +1293,9 @@ void Engine::decoder_body(bool reorder) {
     count(sb.reorder ? "step begin (reorder+embed+LN)" : "step begin (embed+LN)");
   } else {
     if (reorder) {
-      launch_beam_reorder(beam_, stream_);
+      BeamDev bd = beam_;
+      bd.tr_b = next_trace("beam reorder");
+      launch_beam_reorder(bd, stream_);
       count("beam reorder");
     }
     launch_embed_tgt(row_prev_.get(), dr, R, step_.get(), tgt_embed_f32_.get(), nullptr,
@@ -1286,20 +1307,26 @@ void Engine::decoder_body(bool reorder) {
   for (int l = 0; l < c.num_decoder_layers; ++l) {
     DecLayer& L = dec_[l];
     if (l > 0) ln_dec(L.n1);
+    cur_tr_ = next_trace("gemm qkv");
     gemm(act_d_, L.self_qkv, R, dr, qkv_cache_[l].get(), 3 * d, nullptr, nullptr, 0,
          static_cast<long long>(R) * 3 * d, step_.get());
     launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
-                              step_.get(), d_, heads_, scale, dec_ctx_.get(), d, od, stream_);
+                              step_.get(), d_, heads_, scale, dec_ctx_.get(), d,
+                              tr_od("self attention"), stream_);
     count("self attention");
+    cur_tr_ = next_trace("gemm wo (+res)");
     gemm(act_d_, L.self_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
     ln_dec(L.n2);
+    cur_tr_ = next_trace("gemm cross wq");
     gemm(act_d_, L.cross_q, R, dr, dec_cq_.get(), d, nullptr, nullptr, 0);
     launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
-                               enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d, od,
-                               stream_);
+                               enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d,
+                               tr_od("cross attention"), stream_);
     count("cross attention");
+    cur_tr_ = next_trace("gemm cross wo (+res)");
     gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
     ln_dec(L.n3);
+    cur_tr_ = next_trace("gemm w1 (+b1, relu)");
     if (prec_is_tf32x3(act_ff_.prec)) {  // FFN-up writes the FFN-down operand itself
       gemm(act_d_, L.w1, R, dr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
            nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
@@ -1307,15 +1334,19 @@ void Engine::decoder_body(bool reorder) {
       gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
       prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
     }
+    cur_tr_ = next_trace("gemm w2 (+b2, res)");
     gemm(act_ff_, L.w2, R, dr, dec_y_.get(), d, L.b2.get(), dec_y_.get(), 0);
   }
   if (c.num_decoder_layers > 0) {
-    const OperandOut ol = opout(logits_act());
+    OperandOut ol = opout(logits_act());
+    ol.tr = next_trace("layernorm (final)");
     launch_layernorm(dec_y_.get(), d, R, dr, d_, dec_final_.g.get(), dec_final_.b.get(), final_y,
                      d, nullptr, &ol, stream_);
     count("layernorm");
   }
+  cur_tr_ = next_trace("logits gemm + partials");
   if (!use_shortlist_) gemm_logits(R, dr);  // shortlists project inside their top-k kernel
+  cur_tr_ = KTrace{};
 }
 
 void Engine::ensure_step_graph() {
@@ -1449,18 +1480,13 @@ void Engine::capture_one_step() {
       return e ? std::atoi(e) : 8;
     }();
     if (fused_tail && beam_.N >= fused_min_n) {
-      if (small_path()) {
-        bd.tr_a = next_trace("fused top-k + select");
-        next_trace("(unused)");
-      }
+      bd.tr_a = next_trace("fused top-k + select");
       launch_topk_select(logits_.get(), Vp_, part_m_.get(), part_s_.get(), part_arg_.get(),
                          part_ld_, use_shortlist_ ? &sla : nullptr, sl_prec, bd, stream_);
       count("top-k + beam select");
     } else {
-      if (small_path()) {
-        bd.tr_a = next_trace("softmax + top-k");
-        bd.tr_b = next_trace("beam select");
-      }
+      bd.tr_a = next_trace("softmax + top-k");
+      bd.tr_b = next_trace("beam select");
       if (use_shortlist_) {
         launch_shortlist_topk(sl_prec, sla, bd, stream_);
         count("shortlist logits + softmax + top-k");

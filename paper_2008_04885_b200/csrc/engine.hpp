@@ -133,10 +133,12 @@ class Engine {
   DeviceBuffer<int> gemv_sem_;        // split-K tickets (zero between launches)
   // MTG_TRACE=1: in-graph timeline of the small-batch step kernels.
   bool trace_ = false;
+  static constexpr int kTraceSlots = 48;  // timeline slots per decode step
   DeviceBuffer<unsigned long long> trace_buf_;
   int trace_slot_ = 0, trace_per_step_ = 0;
   std::vector<std::string> trace_names_;
   KTrace next_trace(const char* name);
+  KTrace cur_tr_;  // consumed by the next gemm() / gemm_logits() launch
   void trace_reset();
   std::string trace_report();
   void decode_loop(int t_run);

@@ -63,6 +63,7 @@ struct GemmEpilogue {
   // Optional: write the output as a TF32x3 operand, C = tf32(y), C_lo = y - C
   // (the next GEMM's A), instead of plain y.
   float* C_lo;
+  KTrace tr;  // MTG_TRACE timeline slot
 };
 
 // Stores y at C[off] (or its tf32 hi / lo split for the kEpiTf32Out epilogue).
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   }
   pdl_wait();
   pdl_trigger();
+  trace_begin(ep.tr);
   const int M = ep.d_M ? *ep.d_M : ep.M;
   if (m0 >= M) {  // uniform across the CTA
     if (warp == 0 && lane == 0) {  // let the prefetched weight stages land first
@@ -605,6 +607,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+  trace_end(ep.tr);
 }
 
 }  // namespace mtg

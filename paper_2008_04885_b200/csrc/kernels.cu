@@ -183,6 +183,7 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
                                      int has_op) {
   pdl_wait();
   pdl_trigger();
+  trace_begin(op.tr);
   const int rows = d_rows ? *d_rows : max_rows;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -197,6 +198,7 @@ __global__ void layernorm_reg_kernel(const float* __restrict__ x, long long ldx,
     bv[i] = c < n ? b[c] : 0.0f;
   }
   ln_row_regs<KPL>(xv, gv, bv, n, lane, r, y, ldy, rowmax, op, has_op);
+  trace_end(op.tr);
 }
 
 // First kernel of a decode step, one warp per live row r:
@@ -755,6 +757,7 @@ __global__ void __launch_bounds__(256, 3)
                               float* __restrict__ ctx, long long ldc, OperandOut op) {
   pdl_wait();
   pdl_trigger();
+  trace_begin(op.tr);
   extern __shared__ __align__(16) float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
@@ -789,6 +792,7 @@ __global__ void __launch_bounds__(256, 3)
   }
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
+  trace_end(op.tr);
 }
 
 // Decoder cross-attention over the sentence's encoder keys/values.
@@ -801,6 +805,7 @@ __global__ void __launch_bounds__(256, 3)
                                float* __restrict__ ctx, long long ldc, OperandOut op) {
   pdl_wait();
   pdl_trigger();
+  trace_begin(op.tr);
   extern __shared__ __align__(16) float sm[];
   const int r = blockIdx.x;
   if (r >= *d_rows) return;
@@ -829,6 +834,7 @@ __global__ void __launch_bounds__(256, 3)
   }
   __syncthreads();
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
+  trace_end(op.tr);
 }
 
 }  // namespace

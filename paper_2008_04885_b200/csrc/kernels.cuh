@@ -25,6 +25,7 @@ struct OperandOut {
   float* hi = nullptr;
   float* lo = nullptr;
   int* nonfinite = nullptr;
+  KTrace tr;  // MTG_TRACE timeline slot of the kernel writing this operand
 };
 
 // Empty dependent kernel (148 CTAs): the PDL launch floor, for timing.

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(64 + EG * 256, 1)
 
   pdl_wait();
   pdl_trigger();
+  trace_begin(ep.tr);
   const int M = ep.d_M ? *ep.d_M : ep.M;
   const int m_live = (M + 127) / 128;
   const int total = m_live * n_tiles;
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(64 + EG * 256, 1)
     tc_fence_after();
     tmem_dealloc<2 * kTmemCols>(tmem);
   }
+  trace_end(ep.tr);
 }
 
 }  // namespace mtg

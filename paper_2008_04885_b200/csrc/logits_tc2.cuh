@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(320, 1)
 
   pdl_wait();
   pdl_trigger();
+  trace_begin(ep.tr);
   const int M = ep.d_M ? *ep.d_M : ep.M;
   const int m_pairs = (M + 255) / 256;
   const int total = m_pairs * n_tiles;
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_after();
     pair2::tmem_dealloc2<2 * kTmemCols>(tmem);
   }
+  trace_end(ep.tr);
 }
 
 }  // namespace mtg
