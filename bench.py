@@ -285,6 +285,18 @@ def run_gpu(args):
             lat.append((time.perf_counter() - t0) * 1000)
         extra["p90_batch1_ms"] = mt.percentile(lat, 90.0)
         extra["p50_batch1_ms"] = mt.percentile(lat, 50.0)
+        # Batch-1 (small-batch GEMV path) kernels, each chained 50x in one CUDA
+        # graph with PDL on the last batch-1 workspace: in-graph time per launch
+        # and its weight / KV bytes against the HBM roofline.
+        b1 = {}
+        for kid, name in ((13, "gemv_logits_partials"), (12, "gemv_ln_w1"), (11, "gemv_wo"),
+                          (16, "self_attention_t56")):
+            rc = mt.lib().mtg_time_kernel(model._h, kid, 50, ctypes.byref(ms), ctypes.byref(by),
+                                          ctypes.byref(fl))
+            if rc == 0:
+                gbs = by.value / (ms.value * 1e-3) / 1e9
+                b1[name] = dict(us=ms.value * 1e3, bytes=by.value, gbs=gbs, hbm_frac=gbs / hbm_peak)
+        extra["batch1_kernels"] = b1
         # CPU baseline: oracle port, bounded sample, all host threads
         if world == 1 and not args.no_cpu_baseline:
             sys.path.insert(0, os.path.join(ROOT, "tests"))

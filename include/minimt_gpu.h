@@ -177,7 +177,12 @@ void* mtg_model_stream(const mtg_model* m);
  * (kernel: 0 = decoder output-projection GEMM, 1 = log-softmax/top-k,
  * 2 = decoder self-attention, 3 = encoder FFN w1 GEMM) with CUDA events on
  * the handle's stream. Writes the mean milliseconds per launch and the
- * algorithmic bytes and FLOPs of one launch. */
+ * algorithmic bytes and FLOPs of one launch. Small-batch (<= 8 live rows)
+ * step kernels, chained `iters` times in one CUDA graph with programmatic
+ * dependent launch: 10 = empty kernel (launch floor), 11 = Wo GEMV + residual,
+ * 12 = LayerNorm + W1 GEMV, 13 = LayerNorm + output projection + softmax
+ * partials, 14 = batched self-attention, 15 = log-softmax/top-k merge,
+ * 16 = small-batch self-attention, 17 = small-batch cross-attention. */
 int mtg_time_kernel(mtg_model* m, int kernel, int iters, float* ms_per_launch,
                     double* bytes_per_launch, double* flops_per_launch);
 
