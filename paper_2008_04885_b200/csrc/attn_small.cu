@@ -205,12 +205,148 @@ __global__ void __launch_bounds__(kAttnThreads)
   trace_end(a.trace);
 }
 
+// Batched cross-attention, one CTA per (sentence, head), one warp per live
+// beam row of the sentence. The sentence's encoder keys / values of the head
+// are staged once for all its rows, before the programmatic-dependency wait
+// (the beam state that locates them is written two or more kernels back);
+// after the wait each warp loads its query and attends. Same arithmetic as
+// kernels.cu attend_warp_staged64. Writes the fp32 context and, element by
+// element, the next GEMM's bf16 / TF32x3 operand (int8 needs whole-row scales
+// and keeps the per-row kernel).
+struct AttnCrossArgs {
+  const float* cq;
+  long long ldq;
+  const float* ckv;
+  const int* enc_off;
+  const int* enc_len;
+  const int* sent_row0;
+  const int* sent_live;
+  const int* sent_done;
+  int d;
+  float scale;
+  float* ctx;
+  long long ldc;
+  OperandOut op;
+};
+
+__global__ void __launch_bounds__(512)
+    attn_cross_sent_kernel(const AttnCrossArgs a, int max_src) {
+  extern __shared__ __align__(16) float sm[];
+  const int s = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int d = a.d;
+  float* K = sm;
+  float* V = K + max_src * kDh;
+  const int wstride = kDh + (max_src + 3) / 4 * 4;          // 16-byte aligned per-warp blocks
+  float* wq = V + max_src * kDh + warp * wstride;  // [64] query, then [max_src] scores
+  float* ws = wq + kDh;
+  // ---- before the wait: beam state (previous step's selection) and keys ----
+  const int live = a.sent_done[s] ? 0 : a.sent_live[s];
+  const int r0 = a.sent_row0[s];
+  const int n = a.enc_len[s];
+  if (live > 0) {
+    const float* kv = a.ckv + static_cast<long long>(a.enc_off[s]) * 2 * d + h * kDh;
+    stage_kv(
+        K, V, 0, n, [&](int j) { return kv + static_cast<long long>(j) * 2 * d; },
+        [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; });
+  }
+  pdl_wait();
+  pdl_trigger();
+  trace_begin(a.op.tr);
+  cp_async_wait_all();
+  __syncthreads();  // keys / values staged by every thread's copies
+  for (int w = warp; w < live; w += nw) {
+    const long long r = r0 + w;
+    for (int c = lane; c < kDh; c += 32) wq[c] = a.cq[r * a.ldq + h * kDh + c];
+    __syncwarp();
+    // scores (P3): lane per key, dot over the head dimension in order, x scale
+    float mx = -__int_as_float(0x7f800000);
+    for (int j = lane; j < n; j += 32) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int c4 = 0; c4 < 16; ++c4) {
+        const float4 kv = *reinterpret_cast<const float4*>(K + swz(j, c4));
+        const float4 qv = *reinterpret_cast<const float4*>(wq + 4 * c4);
+        acc = __fadd_rn(acc, __fmul_rn(qv.x, kv.x));
+        acc = __fadd_rn(acc, __fmul_rn(qv.y, kv.y));
+        acc = __fadd_rn(acc, __fmul_rn(qv.z, kv.z));
+        acc = __fadd_rn(acc, __fmul_rn(qv.w, kv.w));
+      }
+      const float v = __fmul_rn(acc, a.scale);
+      ws[j] = v;
+      mx = fmaxf(mx, v);
+    }
+    mx = warp_allmax(mx);
+    float part = 0.0f;  // P1: lane-strided keys in order, then the butterfly
+    for (int j = lane; j < n; j += 32) {
+      const float e = det_expf_nonpos(__fsub_rn(ws[j], mx));
+      ws[j] = e;
+      part = __fadd_rn(part, e);
+    }
+    const float sum = warp_allsum(part);
+    for (int j = lane; j < n; j += 32) ws[j] = __fdiv_rn(ws[j], sum);
+    __syncwarp();
+    // context: lane owns columns lane and lane + 32, keys in order
+    float acc_a = 0.0f, acc_b = 0.0f;
+    for (int j = 0; j < n; ++j) {
+      const float p = ws[j];
+      acc_a = __fadd_rn(acc_a, __fmul_rn(p, V[swz(j, lane >> 2) + (lane & 3)]));
+      acc_b = __fadd_rn(acc_b, __fmul_rn(p, V[swz(j, 8 + (lane >> 2)) + (lane & 3)]));
+    }
+    const float vals[2] = {acc_a, acc_b};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const long long c = h * kDh + lane + 32 * u;
+      const float v = vals[u];
+      a.ctx[r * a.ldc + c] = v;
+      const OperandOut& o = a.op;
+      if (o.prec == 1) {
+        o.h[r * o.k_pad + c] = __float2bfloat16_rn(v);
+      } else if (o.prec == 3) {
+        o.hi[r * o.k_pad + c] = v;
+      } else if (o.prec == 2) {
+        uint32_t hb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+        o.hi[r * o.k_pad + c] = __uint_as_float(hb);
+        o.lo[r * o.k_pad + c] = __fsub_rn(v, __uint_as_float(hb));
+      }
+    }
+    __syncwarp();
+  }
+  trace_end(a.op.tr);
+}
+
 size_t attn_small_smem(int keys) {
   return sizeof(float) * (2 * size_t(keys) * kDh + 2 * kDh + size_t(keys)) +
          sizeof(int) * size_t(keys);
 }
 
 }  // namespace
+
+size_t attn_cross_sent_smem(int max_src, int warps) {
+  return sizeof(float) * (2 * size_t(max_src) * kDh + size_t(warps) * (kDh + (max_src + 3) / 4 * 4));
+}
+
+bool attn_cross_sent_supported(int d, int heads, int max_src, int beam) {
+  return heads > 0 && d == heads * kDh && beam <= 16 &&
+         attn_cross_sent_smem(max_src, beam) <= 100 * 1024;
+}
+
+void launch_attn_cross_sent(const float* cq, long long ldq, const float* ckv, const int* enc_off,
+                            const int* enc_len, const int* sent_row0, const int* sent_live,
+                            const int* sent_done, int n_sent, int beam, int max_src, int d,
+                            int heads, float scale, float* ctx, long long ldc,
+                            const OperandOut& op, cudaStream_t st) {
+  if (n_sent <= 0) return;
+  if (op.prec == 0) fail(kStateError, "cross attention per sentence: no int8 operand rows");
+  AttnCrossArgs a{cq, ldq, ckv, enc_off, enc_len, sent_row0, sent_live, sent_done, d, scale, ctx,
+                  ldc, op};
+  const int warps = std::max(1, std::min(beam, 16));
+  const size_t smem = attn_cross_sent_smem(max_src, warps);
+  ensure_smem_attr(attn_cross_sent_kernel, smem);
+  launch_k(attn_cross_sent_kernel, dim3(n_sent, heads), warps * 32, smem, st, a, max_src);
+  MTG_CUDA(cudaGetLastError());
+}
 
 bool attn_small_supported(int d, int heads, int T, int max_src) {
   return heads > 0 && d == heads * kDh && attn_small_smem(std::max(T, max_src)) <= 200 * 1024;

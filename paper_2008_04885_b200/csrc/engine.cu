@@ -1304,6 +1304,14 @@ void Engine::decoder_body(bool reorder) {
     count("embed_tgt");
     ln_dec(ln0, c.num_decoder_layers == 0 ? final_y : nullptr);
   }
+  // Cross-attention per (sentence, head) with the keys staged before the
+  // dependency wait (fp32 / bf16; MTG_CROSS_SENT=0: per row, A/B).
+  static const bool cross_sent_env = [] {
+    const char* e = std::getenv("MTG_CROSS_SENT");
+    return !(e && e[0] == '0');
+  }();
+  const bool cross_sent = cross_sent_env && prec_ != kINT8 &&
+                          attn_cross_sent_supported(d_, heads_, std::max(staged_max_src_, 1), beam_.B);
   for (int l = 0; l < c.num_decoder_layers; ++l) {
     DecLayer& L = dec_[l];
     if (l > 0) ln_dec(L.n1);
@@ -1319,9 +1327,16 @@ void Engine::decoder_body(bool reorder) {
     ln_dec(L.n2);
     cur_tr_ = next_trace("gemm cross wq");
     gemm(act_d_, L.cross_q, R, dr, dec_cq_.get(), d, nullptr, nullptr, 0);
-    launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(), enc_off_.get(),
-                               enc_len_.get(), dr, R, T_, d_, heads_, scale, dec_ctx_.get(), d,
-                               tr_od("cross attention"), stream_);
+    if (cross_sent) {
+      launch_attn_cross_sent(dec_cq_.get(), d, ckv_[l].get(), enc_off_.get(), enc_len_.get(),
+                             sent_row0_.get(), sent_live_.get(), sent_done_.get(), beam_.N,
+                             beam_.B, std::max(staged_max_src_, 1), d_, heads_, scale,
+                             dec_ctx_.get(), d, tr_od("cross attention (per sentence)"), stream_);
+    } else {
+      launch_dec_cross_attention(dec_cq_.get(), d, ckv_[l].get(), row_sent_.get(),
+                                 enc_off_.get(), enc_len_.get(), dr, R, T_, d_, heads_, scale,
+                                 dec_ctx_.get(), d, tr_od("cross attention"), stream_);
+    }
     count("cross attention");
     cur_tr_ = next_trace("gemm cross wo (+res)");
     gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
@@ -1359,6 +1374,7 @@ void Engine::ensure_step_graph() {
   key.shortlist = use_shortlist_;
   key.sl_ids = sl_ids_.get();
   key.sl_off = sl_off_.get();
+  key.max_src = staged_max_src_;
   if (step_exec_ && key == step_key_) return;
   if (step_exec_) cudaGraphExecDestroy(step_exec_);
   if (step_graph_) cudaGraphDestroy(step_graph_);

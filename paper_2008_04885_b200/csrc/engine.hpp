@@ -269,13 +269,14 @@ class Engine {
   int64_t step_kernels_ = 0;
   int ws_gen_ = 0;
   struct StepKey {
-    int n = -1, b = -1, r_max = -1, gen = -1;
+    int n = -1, b = -1, r_max = -1, gen = -1, max_src = -1;
     float alpha = 0.0f;
     bool shortlist = false;
     const void* sl_ids = nullptr;  // graph kernels capture these pointers
     const void* sl_off = nullptr;
     bool operator==(const StepKey& o) const {
-      return n == o.n && b == o.b && r_max == o.r_max && gen == o.gen && alpha == o.alpha &&
+      return n == o.n && b == o.b && r_max == o.r_max && gen == o.gen && max_src == o.max_src &&
+             alpha == o.alpha &&
              shortlist == o.shortlist && sl_ids == o.sl_ids && sl_off == o.sl_off;
     }
   } step_key_;

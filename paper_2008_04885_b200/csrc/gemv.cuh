@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "kernels.cuh"
 #include "launch.cuh"
 
 namespace mtg {
@@ -102,6 +103,15 @@ void launch_gemv_pack(const void* w, int n, int k_pad, int elem, void* out, cuda
 // dim 64, keys / values prefetched before the programmatic-dependency wait;
 // fp32 contexts only (the consuming GEMV builds the operand).
 bool attn_small_supported(int d, int heads, int T, int max_src);
+// Batched cross-attention (fp32 / bf16 operands), CTA per (sentence, head),
+// warp per live beam row; the sentence's keys / values staged once, before
+// the programmatic-dependency wait (attn_small.cu).
+bool attn_cross_sent_supported(int d, int heads, int max_src, int beam);
+void launch_attn_cross_sent(const float* cq, long long ldq, const float* ckv, const int* enc_off,
+                            const int* enc_len, const int* sent_row0, const int* sent_live,
+                            const int* sent_done, int n_sent, int beam, int max_src, int d,
+                            int heads, float scale, float* ctx, long long ldc,
+                            const OperandOut& op, cudaStream_t st);
 // hist != 0 (layer 0 of a beam step): also writes the step's ancestry /
 // token-history rows (the beam reorder), off the step's critical path.
 void launch_attn_small_self(const float* cache, int r_max, int T, int* anc0, int* anc1,

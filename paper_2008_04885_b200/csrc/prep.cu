@@ -1,5 +1,7 @@
 #include "prep.cuh"
 
+#include <cstdint>
+
 #include "errors.hpp"
 #include "launch.cuh"
 
@@ -91,6 +93,53 @@ __global__ void quantize_rows_kernel(const float* __restrict__ x, long long ld_x
   const float scale = scale_of(m);
   int8_t* qr = q + static_cast<long long>(r) * k_pad;
   for (int c = lane; c < k_pad; c += 32) qr[c] = c < k ? quant1(xr[c], scale) : 0;
+  if (lane == 0) row_scale[r] = scale;
+}
+
+// Register-resident variant with float4 loads (k % 4 == 0, k <= 128 * V4,
+// 16-byte aligned rows): lane owns elements 4 lane + 128 i, quantizes them
+// into one 32-bit store (the FFN-down operand at batch 64: 2048 values).
+template <int V4>
+__global__ void quantize_rows_vec_kernel(const float* __restrict__ x, long long ld_x, int k,
+                                         int max_rows, const int* d_rows,
+                                         int8_t* __restrict__ q, int k_pad,
+                                         float* __restrict__ row_scale, int* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
+  const int rows = d_rows ? *d_rows : max_rows;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + r * ld_x;
+  float4 v[V4];
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c = 4 * lane + 128 * i;
+    v[i] = c < k ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float m = 0.0f;
+  int bad = 0;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    bad |= !isfinite(v[i].x) | !isfinite(v[i].y) | !isfinite(v[i].z) | !isfinite(v[i].w);
+    m = fmaxf(fmaxf(m, fmaxf(fabsf(v[i].x), fabsf(v[i].y))), fmaxf(fabsf(v[i].z), fabsf(v[i].w)));
+  }
+  m = warp_max(m);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+  const float scale = scale_of(m);
+  int8_t* qr = q + static_cast<long long>(r) * k_pad;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c = 4 * lane + 128 * i;
+    if (c < k_pad) {
+      const uint32_t w = static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].x, scale))) |
+                         (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].y, scale))) << 8) |
+                         (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].z, scale))) << 16) |
+                         (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].w, scale))) << 24);
+      *reinterpret_cast<uint32_t*>(qr + c) = w;  // columns >= k hold 0 (quantized zeros)
+    }
+  }
+  for (int c = 128 * V4 + 4 * lane; c < k_pad; c += 128) *reinterpret_cast<uint32_t*>(qr + c) = 0u;
   if (lane == 0) row_scale[r] = scale;
 }
 
@@ -198,7 +247,17 @@ void launch_quantize_rows(const float* x, long long ld_x, int k, int max_rows,
   const int wpb = 8;
   const dim3 grid((max_rows + wpb - 1) / wpb), block(wpb * 32);
   const int kpl = (k + 31) / 32;
-  if (kpl <= 16)
+  const bool vec = k % 4 == 0 && ld_x % 4 == 0 && k_pad % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(q) % 4 == 0;
+  if (vec && k <= 512) {
+    const dim3 g4((max_rows + 3) / 4), b4(4 * 32);  // more, smaller CTAs
+    launch_k(quantize_rows_vec_kernel<4>, g4, b4, 0, st, x, ld_x, k, max_rows, d_rows, q, k_pad,
+             row_scale, nonfinite_flag);
+  } else if (vec && k <= 2048) {
+    const dim3 g4((max_rows + 3) / 4), b4(4 * 32);
+    launch_k(quantize_rows_vec_kernel<16>, g4, b4, 0, st, x, ld_x, k, max_rows, d_rows, q, k_pad,
+             row_scale, nonfinite_flag);
+  } else if (kpl <= 16)
     launch_k(quantize_rows_reg_kernel<16>, grid, block, 0, st, x, ld_x, k, max_rows, d_rows, q, k_pad,
                                                          row_scale, nonfinite_flag);
   else if (kpl <= 64)
