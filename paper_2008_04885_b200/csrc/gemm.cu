@@ -179,6 +179,12 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
       bn = kLongKBn;
     bn = std::max(bn, min_bn);
   }
+  // fp32 FFN-up at batch 64 (N = 4K, three m tiles): 64-column tiles, unsplit,
+  // with the one-CTA-per-SM pipeline (more operand bytes in flight per CTA):
+  // measured 16.5 -> 14.2 us per launch in the step graph (tools/step_trace.py).
+  const bool ffn_up_deep = !force_bn && bn == 32 && prec_is_tf32x3(b.prec) && p.m_tiles >= 3 &&
+                           n >= 4 * a.k_pad && a.k_pad >= 256;
+  if (ffn_up_deep) bn = 64;
   p.bn = bn;
   p.n_tiles = (n + bn - 1) / bn;
   // Split-K over a z cluster when the output tiles cannot fill the SMs and a
@@ -200,7 +206,16 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   const int tiles = p.m_tiles * p.n_tiles;
   const long long tile_bytes = static_cast<long long>(p.num_kb) * gemm_stage_bytes(a.prec, bn);
   const int by_bytes = static_cast<int>((tile_bytes + split_bytes - 1) / split_bytes);
-  if (allow_split && tiles < 148 && p.num_kb >= 4 && by_bytes > 1)
+  // MTG_GEMM_DEEP="NxK,..." (A/B): these shapes run unsplit with the deepest
+  // one-CTA-per-SM pipeline.
+  static const std::string deep_map = [] {
+    const char* e = std::getenv("MTG_GEMM_DEEP");
+    return std::string(e ? e : "");
+  }();
+  const bool deep = ffn_up_deep || (!deep_map.empty() && deep_map.find(std::to_string(n) + "x" +
+                                                                      std::to_string(a.k_pad)) !=
+                                                         std::string::npos);
+  if (allow_split && !deep && tiles < 148 && p.num_kb >= 4 && by_bytes > 1)
     p.splits = std::max(1, std::min({p.num_kb / 2, split_ctas / tiles, 8, by_bytes}));
   // Pipeline depth: no deeper than the K loop, and shallow enough for two
   // CTAs per SM when the tile allows it (epilogue / mainloop overlap, and the
@@ -210,7 +225,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   const int want = std::min(kMaxStages, std::max(2, p.num_kb));
   const int two_per_sm = (113 * 1024 - kGemmSmemExtra) / stage;
   const int one_per_sm = (227 * 1024 - kGemmSmemExtra) / stage;
-  p.nst = std::min(want, two_per_sm >= 2 ? two_per_sm : one_per_sm);
+  p.nst = std::min(want, two_per_sm >= 2 && !deep ? two_per_sm : one_per_sm);
   if (p.nst < 2 || p.nst * stage < kEpiStageBytes) fail(kStateError, "gemm: tile too large");
   if (p.splits > 1) {  // the parked split-K partial tile follows the epilogue staging
     const int need = kEpiStageBytes + 128 * (bn + 4) * 4;
