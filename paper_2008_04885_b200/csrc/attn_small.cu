@@ -16,6 +16,7 @@
 // P1 softmax over lane-strided keys, contexts summed in key order.
 #include <algorithm>
 
+#include "attn_warp.cuh"
 #include "detmath.cuh"
 #include "errors.hpp"
 #include "gemv.cuh"
@@ -27,31 +28,7 @@ namespace mtg {
 namespace {
 
 constexpr int kAttnThreads = 128;
-constexpr int kDh = 64;
-
-__device__ __forceinline__ void cp_async16s(float* smem_dst, const float* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-
-// Row j of a [keys][64] block, 16-byte chunk c stored at chunk c ^ (j & 15):
-// lane-per-key reads and column-per-thread reads are both conflict-free.
-__device__ __forceinline__ int swz(int j, int c4) { return j * kDh + ((c4 ^ (j & 15)) << 2); }
-
-// Copies key / value rows [j0, j1) (row pointers from kp / vp) into K / V.
-template <class KP, class VP>
-__device__ __forceinline__ void stage_kv(float* K, float* V, int j0, int j1, KP kp, VP vp) {
-  for (int i = threadIdx.x; i < (j1 - j0) * 16; i += blockDim.x) {
-    const int j = j0 + (i >> 4), c4 = i & 15;
-    cp_async16s(K + swz(j, c4), kp(j) + 4 * c4);
-    cp_async16s(V + swz(j, c4), vp(j) + 4 * c4);
-  }
-}
+constexpr int kDh = kAttnDh;
 
 struct AttnSmallArgs {
   int self_mode;  // 1: self-attention over the KV cache, 0: cross-attention
@@ -253,46 +230,16 @@ __global__ void __launch_bounds__(512)
   pdl_wait();
   pdl_trigger();
   trace_begin(a.op.tr);
+  if (threadIdx.x == 0) trace_phase(a.op.tr, 0);
   cp_async_wait_all();
   __syncthreads();  // keys / values staged by every thread's copies
+  if (threadIdx.x == 0) trace_phase(a.op.tr, 1);
   for (int w = warp; w < live; w += nw) {
     const long long r = r0 + w;
     for (int c = lane; c < kDh; c += 32) wq[c] = a.cq[r * a.ldq + h * kDh + c];
     __syncwarp();
-    // scores (P3): lane per key, dot over the head dimension in order, x scale
-    float mx = -__int_as_float(0x7f800000);
-    for (int j = lane; j < n; j += 32) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int c4 = 0; c4 < 16; ++c4) {
-        const float4 kv = *reinterpret_cast<const float4*>(K + swz(j, c4));
-        const float4 qv = *reinterpret_cast<const float4*>(wq + 4 * c4);
-        acc = __fadd_rn(acc, __fmul_rn(qv.x, kv.x));
-        acc = __fadd_rn(acc, __fmul_rn(qv.y, kv.y));
-        acc = __fadd_rn(acc, __fmul_rn(qv.z, kv.z));
-        acc = __fadd_rn(acc, __fmul_rn(qv.w, kv.w));
-      }
-      const float v = __fmul_rn(acc, a.scale);
-      ws[j] = v;
-      mx = fmaxf(mx, v);
-    }
-    mx = warp_allmax(mx);
-    float part = 0.0f;  // P1: lane-strided keys in order, then the butterfly
-    for (int j = lane; j < n; j += 32) {
-      const float e = det_expf_nonpos(__fsub_rn(ws[j], mx));
-      ws[j] = e;
-      part = __fadd_rn(part, e);
-    }
-    const float sum = warp_allsum(part);
-    for (int j = lane; j < n; j += 32) ws[j] = __fdiv_rn(ws[j], sum);
-    __syncwarp();
-    // context: lane owns columns lane and lane + 32, keys in order
-    float acc_a = 0.0f, acc_b = 0.0f;
-    for (int j = 0; j < n; ++j) {
-      const float p = ws[j];
-      acc_a = __fadd_rn(acc_a, __fmul_rn(p, V[swz(j, lane >> 2) + (lane & 3)]));
-      acc_b = __fadd_rn(acc_b, __fmul_rn(p, V[swz(j, 8 + (lane >> 2)) + (lane & 3)]));
-    }
+    float acc_a, acc_b;
+    attend_warp64(K, V, wq, ws, n, a.scale, lane, acc_a, acc_b);
     const float vals[2] = {acc_a, acc_b};
 #pragma unroll
     for (int u = 0; u < 2; ++u) {

@@ -224,7 +224,10 @@ Engine::Engine(HostModel model, int precision, int device)
     fail(kUsageError, "unknown precision " + std::to_string(prec_));
   if (host_.quantized && prec_ != kINT8) prec_ = kINT8;  // tools/minimt.cpp:317-320
   if (const char* e = std::getenv("MTG_DIAG_EVENTS")) diag_ = e[0] == '1';
-  if (const char* e = std::getenv("MTG_TRACE")) trace_ = e[0] == '1';
+  if (const char* e = std::getenv("MTG_TRACE")) {
+    trace_ = e[0] == '1' || e[0] == '2';
+    trace_phases_ = e[0] == '2';
+  }
   if (const char* e = std::getenv("MTG_NO_SPLIT_K")) split_k_ = e[0] != '1';
   if (prec_ == kINT8 && !host_.quantized) quantize_weights(host_);
   const ModelConfig& c = host_.config;
@@ -999,6 +1002,7 @@ KTrace Engine::next_trace(const char* name) {
   if (trace_slot_ >= per) return k;
   if (static_cast<int>(trace_names_.size()) <= trace_slot_) trace_names_.push_back(name);
   k.buf = trace_buf_.get();
+  if (trace_phases_) k.ph = phase_buf_.get();
   k.slot = trace_slot_++;
   k.per_step = per;
   k.d_step = step_.get();
@@ -1013,6 +1017,12 @@ void Engine::trace_reset() {
   std::vector<unsigned long long> init(trace_buf_.size());
   for (size_t i = 0; i < init.size(); ++i) init[i] = (i & 1) ? 0ull : ~0ull;
   trace_buf_.upload(init.data(), init.size(), stream_);
+  if (trace_phases_) {
+    const size_t np = size_t(kTracePhases) * T_ * kTraceSlots;
+    if (phase_buf_.size() < np) phase_buf_.resize(np);
+    std::vector<unsigned long long> z(phase_buf_.size(), 0ull);
+    phase_buf_.upload(z.data(), z.size(), stream_);
+  }
 }
 
 // Per kernel of the step: mean gap from the previous traced kernel's last CTA
@@ -1028,6 +1038,13 @@ std::string Engine::trace_report() {
   auto valid = [&](const unsigned long long* s, int k) { return s[2 * k] != ~0ull && s[2 * k + 1] != 0ull; };
   std::vector<double> gap(per, 0.0), dur(per, 0.0);
   std::vector<int> ngap(per, 0), ndur(per, 0);
+  std::vector<unsigned long long> pb;
+  if (trace_phases_) {
+    pb.resize(phase_buf_.size());
+    phase_buf_.download(pb.data(), pb.size());
+  }
+  std::vector<double> ph(size_t(per) * kTracePhases, 0.0);
+  std::vector<int> nph(size_t(per) * kTracePhases, 0);
   double total = 0.0;
   int steps = 0;
   for (int t = 0; t + 1 < T_; ++t) {
@@ -1039,6 +1056,14 @@ std::string Engine::trace_report() {
       if (first < 0) first = k;
       dur[k] += double(s[2 * k + 1]) - double(s[2 * k]);
       ++ndur[k];
+      if (!pb.empty()) {
+        const unsigned long long* p = pb.data() + (size_t(t) * per + k) * kTracePhases;
+        for (int i = 0; i < kTracePhases; ++i)
+          if (p[i] != 0ull) {
+            ph[size_t(k) * kTracePhases + i] += double(p[i]) - double(s[2 * k]);
+            ++nph[size_t(k) * kTracePhases + i];
+          }
+      }
       if (prev >= 0) {
         gap[k] += double(s[2 * k]) - double(s[2 * prev + 1]);
         ++ngap[k];
@@ -1062,6 +1087,15 @@ std::string Engine::trace_report() {
                   k < static_cast<int>(trace_names_.size()) ? trace_names_[k].c_str() : "?",
                   ngap[k] ? gap[k] / ngap[k] / 1000.0 : 0.0, dur[k] / ndur[k] / 1000.0);
     out += line;
+    std::string pl;
+    for (int i = 0; i < kTracePhases; ++i) {
+      const int n = nph[size_t(k) * kTracePhases + i];
+      if (n == 0) continue;
+      char b2[48];
+      std::snprintf(b2, sizeof b2, " p%d %.2f", i, ph[size_t(k) * kTracePhases + i] / n / 1000.0);
+      pl += b2;
+    }
+    if (!pl.empty()) out += "      phases (us after first start):" + pl + "\n";
   }
   char tl[200];
   std::snprintf(tl, sizeof tl, "  step %.2f us (first kernel's gap: from the previous step's last)\n",

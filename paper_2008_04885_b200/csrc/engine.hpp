@@ -135,6 +135,8 @@ class Engine {
   bool trace_ = false;
   static constexpr int kTraceSlots = 48;  // timeline slots per decode step
   DeviceBuffer<unsigned long long> trace_buf_;
+  DeviceBuffer<unsigned long long> phase_buf_;  // MTG_TRACE=2
+  bool trace_phases_ = false;
   int trace_slot_ = 0, trace_per_step_ = 0;
   std::vector<std::string> trace_names_;
   KTrace next_trace(const char* name);

@@ -6,8 +6,11 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 
 #include "errors.hpp"
@@ -136,6 +139,59 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
   fail(kStateError, "gemm: unsupported tile width");
 }
 
+__global__ void __launch_bounds__(kGemmThreads, 2) occupancy_probe_kernel(int* p) {
+  extern __shared__ int probe_smem[];
+  if (p) p[threadIdx.x] = probe_smem[threadIdx.x];
+}
+
+// CTAs of one split-K GEMM (cluster of `cs` along z, `smem` bytes each) that
+// can be co-resident: clusters must fit inside one GPC, so e.g. at two CTAs
+// per SM only 71 clusters of 4 (284 CTAs) fit, not 74 -- a 288-CTA grid then
+// runs a second wave (measured: +10 us on the fp32 QKV GEMM). Cached per
+// (device, smem, cs).
+int max_cluster_ctas(int smem, int cs) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, int> cache;
+  int dev = 0;
+  MTG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, smem, cs);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  // Queried with a stand-in of the GEMM's launch shape: for the tcgen05
+  // kernels themselves the API reports one CTA per SM, while two run
+  // (ncu: occupancy limited by shared memory at 2 blocks).
+  auto k = occupancy_probe_kernel;
+  ensure_smem_attr(k, 227 * 1024);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, 1, cs);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = cs;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  const int ctas = n * cs;
+  cache[key] = ctas;
+  if (std::getenv("MTG_PLAN_DEBUG")) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kGemmThreads, smem);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k);
+    std::fprintf(stderr, "occupancy smem=%d cs=%d clusters=%d blocks/SM=%d regs=%d maxdyn=%d static=%zu\n",
+                 smem, cs, n, per_sm, fa.numRegs, fa.maxDynamicSharedSizeBytes, fa.sharedSizeBytes);
+  }
+  return ctas;
+}
+
 }  // namespace
 
 // Fewest m tiles for the long-K 64-column rule below (MTG_LONGK_MTILES A/B;
@@ -185,6 +241,12 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   const bool ffn_up_deep = !force_bn && bn == 32 && prec_is_tf32x3(b.prec) && p.m_tiles >= 3 &&
                            n >= 4 * a.k_pad && a.k_pad >= 256;
   if (ffn_up_deep) bn = 64;
+  // Just under one tile per SM at 32 columns (the fused QKV GEMM at batch 64:
+  // 144 tiles, split 2): 64-column tiles split 3-4 ways read the activation
+  // rows half as often (measured int8 5.2 -> 4.5 us, fp32 11.6 -> 11.2 us).
+  if (!force_bn && !ffn_up_deep && bn == 32 && p.m_tiles * ((n + 31) / 32) > 96 &&
+      p.m_tiles * ((n + 31) / 32) < 148)
+    bn = 64;
   p.bn = bn;
   p.n_tiles = (n + bn - 1) / bn;
   // Split-K over a z cluster when the output tiles cannot fill the SMs and a
@@ -198,7 +260,10 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
     const char* e = std::getenv("MTG_SPLIT_CTAS");
     return e ? std::atoi(e) : 0;
   }();
-  const int split_ctas = split_ctas_env > 0 ? split_ctas_env : 296;
+  // CTAs resident per SM with this tile (the pipeline-depth rule below).
+  const int stage_b = gemm_stage_bytes(a.prec, bn);
+  const int per_sm = (113 * 1024 - kGemmSmemExtra) / stage_b >= 2 ? 2 : 1;
+  const int split_ctas = split_ctas_env > 0 ? split_ctas_env : 148 * per_sm;
   static const long long split_bytes = [] {
     const char* e = std::getenv("MTG_SPLIT_KB");
     return (e ? std::atoll(e) : 160LL) * 1024;
@@ -216,7 +281,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
                                                                       std::to_string(a.k_pad)) !=
                                                          std::string::npos);
   if (allow_split && !deep && tiles < 148 && p.num_kb >= 4 && by_bytes > 1)
-    p.splits = std::max(1, std::min({p.num_kb / 2, split_ctas / tiles, 8, by_bytes}));
+    p.splits = std::max(1, std::min({p.num_kb / 2, split_ctas / tiles, kMaxSplits, by_bytes}));
   // Pipeline depth: no deeper than the K loop, and shallow enough for two
   // CTAs per SM when the tile allows it (epilogue / mainloop overlap, and the
   // next kernel's CTAs can start under PDL; measured: a one-CTA-per-SM depth
@@ -233,6 +298,19 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
     if (p.nst * stage < need) p.splits = 1;
   }
   p.smem = p.nst * stage + kGemmSmemExtra;
+  // One wave: fewer splits when the clusters would not all be co-resident.
+  const int splits0 = p.splits;
+  static const bool cluster_cap = [] {
+    const char* e = std::getenv("MTG_CLUSTER_CAP");
+    return !(e && e[0] == '0');
+  }();
+  while (cluster_cap && p.splits > 1 && tiles * p.splits > max_cluster_ctas(p.smem, p.splits))
+    --p.splits;
+  static const bool plan_debug = std::getenv("MTG_PLAN_DEBUG") != nullptr;
+  if (plan_debug)
+    std::fprintf(stderr, "plan n=%d k_pad=%d m=%d bn=%d tiles=%d splits=%d->%d nst=%d smem=%d cap=%d\n",
+                 n, a.k_pad, m_max, bn, tiles, splits0, p.splits, p.nst, p.smem,
+                 splits0 > 1 ? max_cluster_ctas(p.smem, splits0) : -1);
   p.a_box = (p.m_tiles == 1 && !split_a) ? std::max(8, (m_max + 7) / 8 * 8) : 128;
   p.a = make_map(a.ptr, a.prec, a.rows, a.k_pad, p.a_box);
   p.b = make_map(b.ptr, b.prec, b.rows, b.k_pad, bn);
@@ -350,6 +428,11 @@ static void launch_logits_pair(const GemmPlan& p, const GemmEpilogue& ep, cudaSt
 void launch_gemm(const GemmPlan& p, const GemmEpilogue& ep_in, cudaStream_t stream) {
   GemmEpilogue ep = ep_in;
   ep.a_box = p.a_box;
+  static const int split_dist = [] {
+    const char* e = std::getenv("MTG_SPLITK_DIST");
+    return e ? std::atoi(e) : 1;
+  }();
+  ep.split_dist = split_dist;
   if (p.pair) return launch_logits_pair(p, ep, stream);
   if (p.persistent) {
     if (!ep.part_m) fail(kStateError, "logits: softmax partial buffers missing");

@@ -64,6 +64,7 @@ struct GemmEpilogue {
   // (the next GEMM's A), instead of plain y.
   float* C_lo;
   KTrace tr;  // MTG_TRACE timeline slot
+  int split_dist;  // split-K sums by all epilogue threads (1) or per owner warp (0)
 };
 
 // Stores y at C[off] (or its tf32 hi / lo split for the kEpiTf32Out epilogue).
@@ -95,6 +96,7 @@ __host__ __device__ constexpr bool prec_is_tf32x3(int prec) {
 
 constexpr int kMaxSegments = 4;
 constexpr int kMaxStages = 8;
+constexpr int kMaxSplits = 8;  // split-K cluster size (portable cluster limit)
 constexpr int kGemmThreads = 320;
 constexpr int kEpiWarps = 8;
 
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   pdl_wait();
   pdl_trigger();
   trace_begin(ep.tr);
+  if (threadIdx.x == 0) trace_phase(ep.tr, 0);
   const int M = ep.d_M ? *ep.d_M : ep.M;
   if (m0 >= M) {  // uniform across the CTA
     if (warp == 0 && lane == 0) {  // let the prefetched weight stages land first
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         const uint32_t ph = (kb / nst) & 1;
         mbar_wait(kSplitA ? &conv_bar[s] : &full_bar[s], ph);
         tc_fence_after();
+        if (kb == 0) trace_phase(ep.tr, 1);
         const uint32_t a_base = smem_u32(smem + s * kStageBytes);
         const uint32_t b_base = a_base + kATile;
 #pragma unroll
@@ -270,6 +274,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         tc_commit(&empty_bar[s]);  // slot reusable once these MMAs retire
       }
       tc_commit(accum_bar);        // accumulator complete
+      trace_phase(ep.tr, 2);
     }
     __syncwarp();
     if (splits > 1) {
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     float* const Cbase = ep.C + step_off + static_cast<long long>(rbase) * ldc;
     // BN = 32 (the N = d_model residual GEMMs): each epilogue warp owns one
     // 32-row x 16-column chunk, so its residual and bias are fetched while
-    // the MMAs are still running.
+    // the MMAs are still running (measured slower for BN = 64).
     constexpr bool kPrefetch = (BN == 32 && EPI != kEpiSoftmaxParts);
     float res_pre[kPrefetch ? 32 : 1];
     float bias_pre = 0.0f;
@@ -362,11 +367,14 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     int sub_a[kSubs];
     mbar_wait(accum_bar, 0);
     tc_fence_after();
+    if (warp == 2 && lane == 0) trace_phase(ep.tr, 3);
     // Split-K over a thread-block cluster along z: every split parks its raw
-    // accumulator tile in its own (drained) shared memory, then the owner of
-    // each region reads all splits' partials through DSMEM, sums them in z
-    // order (int32 exact, float ordered) and runs the epilogue for it. Two
-    // cluster barriers bracket the reads.
+    // accumulator tile in its own (drained) shared memory; each region of the
+    // tile has an owner split, whose 256 epilogue threads read the region's
+    // partials from all splits through DSMEM (one float4 per thread and
+    // split, all loads in flight together), sum them in z order (int32 exact,
+    // float ordered) into the owner's own parked copy, and then run the
+    // epilogue for it. Two cluster barriers bracket the remote reads.
     constexpr int kPartPitch = BN + 4;  // words; conflict-free row-per-thread float4
     uint32_t* part = reinterpret_cast<uint32_t*>(smem + kEpiStageBytes);
     const uint32_t* my_part_row = part + (q * 32 + lane) * kPartPitch;
@@ -387,16 +395,63 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
               make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
       }
       cluster_sync_all();  // (1) all partials parked
+      if (warp == 2 && lane == 0) trace_phase(ep.tr, 4);
+      // Owned regions g = z, z + splits, ... (region g = row quarter g / 2,
+      // column half g % 2). Other splits read only their own regions of this
+      // CTA's copy, so the sums can overwrite the owned ones in place.
+      constexpr int kQ4 = kHalf / 4;  // float4 per region row
+      constexpr int kPerRegion = 32 * kQ4;
+      const int nreg = ep.split_dist ? (2 * 4 - 1 - z) / splits + 1 : 0;
+      for (int e = threadIdx.x - 64; e < nreg * kPerRegion; e += kEpiWarps * 32) {
+        const int ri = e / kPerRegion, w = e - ri * kPerRegion;
+        const int g = z + ri * splits;
+        const int row = (g >> 1) * 32 + w / kQ4;
+        if (m0 + row >= M) continue;
+        uint32_t* loc = part + row * kPartPitch + (g & 1) * kHalf + (w % kQ4) * 4;
+        const uint32_t addr = smem_u32(loc);
+        uint4 pz[kMaxSplits];
+#pragma unroll
+        for (int zz = 0; zz < kMaxSplits; ++zz)
+          if (zz < splits)
+            pz[zz] = zz == z ? *reinterpret_cast<const uint4*>(loc) : dsmem_ld4(dsmem_map(addr, zz));
+        uint4 a = pz[0];
+#pragma unroll
+        for (int zz = 1; zz < kMaxSplits; ++zz) {
+          if (zz >= splits) break;
+          const uint4 b = pz[zz];
+          if constexpr (PREC == kPrecI8) {
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+          } else {
+            a.x = __float_as_uint(__fadd_rn(__uint_as_float(a.x), __uint_as_float(b.x)));
+            a.y = __float_as_uint(__fadd_rn(__uint_as_float(a.y), __uint_as_float(b.y)));
+            a.z = __float_as_uint(__fadd_rn(__uint_as_float(a.z), __uint_as_float(b.z)));
+            a.w = __float_as_uint(__fadd_rn(__uint_as_float(a.w), __uint_as_float(b.w)));
+          }
+        }
+        *reinterpret_cast<uint4*>(loc) = a;
+      }
+      if (ep.split_dist) asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     }
 #pragma unroll 1
     for (int c = half * kHalf; c < (half + 1) * kHalf; c += kChunk) {
       if (nrows <= 0) break;  // warp-uniform
       uint32_t r[32];
-      if (splits > 1) {
+      if (splits > 1 && ep.split_dist) {  // this region's split sum (above)
+#pragma unroll
+        for (int j = 0; j < kChunk; j += 4) {
+          const uint4 a = *reinterpret_cast<const uint4*>(my_part_row + c + j);
+          r[j] = a.x;
+          r[j + 1] = a.y;
+          r[j + 2] = a.z;
+          r[j + 3] = a.w;
+        }
+      } else if (splits > 1) {  // the owner warp reads every split's partials
         const uint32_t my_addr = smem_u32(my_part_row + c);
 #pragma unroll
         for (int j = 0; j < kChunk; j += 4) {
-          // z order from split 0, whichever split owns the region
           uint4 a = z == 0 ? *reinterpret_cast<const uint4*>(my_part_row + c + j)
                            : dsmem_ld4(dsmem_map(my_addr + 4 * j, 0));
           for (int zz = 1; zz < splits; ++zz) {
@@ -426,6 +481,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
                   *reinterpret_cast<uint32_t(*)[16]>(r));
         tmem_ld_wait();
       }
+      if (lane == 0 && c == half * kHalf) trace_phase(ep.tr, 6);
       if (n0 + c >= N) continue;  // warp-uniform
       if (nrows < 32 && lane >= nrows) {  // rows past M: stale A rows (GemmPlan::a_box)
 #pragma unroll
@@ -549,6 +605,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
       }
       __syncwarp();
     }
+    if (lane == 0) trace_phase(ep.tr, 5);
     if (seg_mode && nrows > 0) {  // constexpr-false for the other epilogues
       // Segmented max over the warp's rows (segments are contiguous row
       // ranges), then one atomic per segment present in the warp.

@@ -30,7 +30,11 @@ struct KTrace {
   int slot = 0;
   int per_step = 0;
   const int* d_step = nullptr;
+  // MTG_TRACE=2: per-phase times (latest CTA to reach phase i), kTracePhases
+  // per (step, slot)
+  unsigned long long* ph = nullptr;
 };
+constexpr int kTracePhases = 8;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -43,6 +47,11 @@ __device__ __forceinline__ void trace_begin(const KTrace& k) {
 __device__ __forceinline__ void trace_end(const KTrace& k) {
   if (k.buf && threadIdx.x == 0)
     atomicMax(&k.buf[2 * (static_cast<long long>(*k.d_step) * k.per_step + k.slot) + 1], gtimer());
+}
+__device__ __forceinline__ void trace_phase(const KTrace& k, int i) {
+  if (k.ph)
+    atomicMax(&k.ph[(static_cast<long long>(*k.d_step) * k.per_step + k.slot) * kTracePhases + i],
+              gtimer());
 }
 // Variants with the step passed in (kernels that advance the step counter).
 __device__ __forceinline__ void trace_begin_at(const KTrace& k, int t) {

@@ -1,7 +1,7 @@
 # In-graph timeline of one batch-1 decode (MTG_TRACE=1): per step kernel,
 # the gap after the previous kernel's last CTA and the kernel's duration.
 import os, sys
-os.environ["MTG_TRACE"] = "1"
+os.environ.setdefault("MTG_TRACE", "1")  # 2: also per-phase times
 sys.path.insert(0, '/root/repo')
 import paper_2008_04885_b200 as mt
 from bench import CONFIG_20_2, sources

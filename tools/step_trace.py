@@ -3,7 +3,7 @@
 # (first post-wait CTA to last CTA exit), averaged over the steps.
 #   python tools/step_trace.py <f32|int8|bf16> [sentences=64]
 import os, sys
-os.environ["MTG_TRACE"] = "1"
+os.environ.setdefault("MTG_TRACE", "1")  # 2: also per-phase times
 sys.path.insert(0, '/root/repo')
 import paper_2008_04885_b200 as mt
 from bench import CONFIG_20_2, sources
