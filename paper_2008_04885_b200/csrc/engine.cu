@@ -1184,8 +1184,10 @@ void Engine::decoder_body_small(bool reorder) {
                              std::min(R, kGemvRows), d_, heads_, scale, dec_ctx_.get(), d, stream_,
                              next_trace("self attention"));
     } else {
+      // the QKV GEMV of layer 0 did the history reorder: no early reads
       launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
-                                step_.get(), d_, heads_, scale, dec_ctx_.get(), d, none, stream_);
+                                step_.get(), d_, heads_, scale, dec_ctx_.get(), d, none, stream_,
+                                l == 0 && reorder ? 0 : 1);
     }
     count("self attention");
     GemvArgs o = gemv_args(L.self_wo);
@@ -1298,6 +1300,21 @@ void Engine::decoder_body(bool reorder) {
     return e ? std::atoi(e) : 0;
   }();
   const bool fused = d_ <= 512 && fusion > 0 && !(use_shortlist_ && c.num_decoder_layers == 0);
+  static const bool fold_env = [] {
+    const char* e = std::getenv("MTG_FOLD_REORDER");
+    return !(e && e[0] == '0');
+  }();
+  const bool fold_reorder = fold_env && !(fused && fusion == 2) && c.num_decoder_layers > 0;
+  HistReorder hist;
+  if (fold_reorder && reorder) {
+    hist.on = 1;
+    hist.anc[0] = anc0_.get();
+    hist.anc[1] = anc1_.get();
+    hist.tok[0] = tok0_.get();
+    hist.tok[1] = tok1_.get();
+    hist.row_parent = row_parent_.get();
+    hist.row_prev = row_prev_.get();
+  }
   const LN& ln0 = c.num_decoder_layers > 0 ? dec_[0].n1 : dec_final_;
   if (fused) {
     StepBegin sb{};
@@ -1313,7 +1330,7 @@ void Engine::decoder_body(bool reorder) {
     sb.x = dec_y_.get();
     sb.ldx = d;
     sb.reorder = reorder && fusion == 2 ? 1 : 0;
-    if (reorder && fusion != 2) {
+    if (reorder && fusion != 2 && !fold_reorder) {
       launch_beam_reorder(beam_, stream_);
       count("beam reorder");
     }
@@ -1326,7 +1343,9 @@ void Engine::decoder_body(bool reorder) {
     launch_step_begin(sb, R, ln0.g.get(), ln0.b.get(), od, stream_);
     count(sb.reorder ? "step begin (reorder+embed+LN)" : "step begin (embed+LN)");
   } else {
-    if (reorder) {
+    // The history reorder runs inside the layer-0 self-attention (before its
+    // dependency wait, off the critical path); MTG_FOLD_REORDER=0: own kernel.
+    if (reorder && !fold_reorder) {
       BeamDev bd = beam_;
       bd.tr_b = next_trace("beam reorder");
       launch_beam_reorder(bd, stream_);
@@ -1354,7 +1373,7 @@ void Engine::decoder_body(bool reorder) {
          static_cast<long long>(R) * 3 * d, step_.get());
     launch_dec_self_attention(qkv_cache_[l].get(), R, T_, anc0_.get(), anc1_.get(), dr,
                               step_.get(), d_, heads_, scale, dec_ctx_.get(), d,
-                              tr_od("self attention"), stream_);
+                              tr_od("self attention"), stream_, 1, l == 0 ? hist : HistReorder{});
     count("self attention");
     cur_tr_ = next_trace("gemm wo (+res)");
     gemm(act_d_, L.self_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);

@@ -754,15 +754,25 @@ __global__ void __launch_bounds__(256, 3)
     dec_self_attention_kernel(const float* __restrict__ cache, int r_max, int T,
                               const int* __restrict__ anc0, const int* __restrict__ anc1,
                               const int* d_rows, const int* d_step, int d, int dh_rt, float scale,
-                              float* __restrict__ ctx, long long ldc, OperandOut op) {
-  pdl_wait();
-  pdl_trigger();
-  trace_begin(op.tr);
+                              float* __restrict__ ctx, long long ldc, OperandOut op, int early,
+                              HistReorder hist) {
   extern __shared__ __align__(16) float sm[];
   const int r = blockIdx.x;
-  if (r >= *d_rows) return;
-  const int dh = DH > 0 ? DH : dh_rt;
+  // early bit 0: before the dependency wait, the row count, step and ancestry
+  // (written by the previous step's tail and the step-start reorder, two or
+  // more kernels back) and an L2 prefetch of the cached keys / values of
+  // positions < t (bit 1; 4 KB per position: k | v of all heads), which the QKV GEMM
+  // running in front of this kernel does not touch. early = 0 (the reorder
+  // ran in the kernel just before): all of it after the wait.
+  if (!early) pdl_wait();
+  const int R = *d_rows;
   const int t = *d_step;
+  if (r >= R) {
+    if (early) pdl_wait();
+    pdl_trigger();
+    return;
+  }
+  const int dh = DH > 0 ? DH : dh_rt;
   // Warp w attends heads w, w + nw, ... (at most 8 warps per CTA).
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int heads = d / dh;
@@ -773,10 +783,34 @@ __global__ void __launch_bounds__(256, 3)
   float* row = sm + nw * W;                      // [d] context row
   float* red = row + d;                          // [33]
   int* arow = reinterpret_cast<int*>(red + 33);  // [T] ancestor rows
-  const int* ar = ((t & 1) ? anc1 : anc0) + static_cast<long long>(r) * T;
-  for (int j = threadIdx.x; j <= t; j += blockDim.x) arow[j] = ar[j];
-  __syncthreads();
   const long long ld3 = 3LL * d;
+  // With the folded reorder (hist.on, early only): positions < t from the
+  // parent's table of step t-1, itself at t; the step's tables are written
+  // here (nothing reads them before this kernel).
+  const bool fold = hist.on && early && t >= 1;
+  const int* ar = fold ? ((t - 1) & 1 ? anc1 : anc0) + static_cast<long long>(hist.row_parent[r]) * T
+                       : ((t & 1) ? anc1 : anc0) + static_cast<long long>(r) * T;
+  int* an = fold ? hist.anc[t & 1] + static_cast<long long>(r) * T : nullptr;
+  if (fold) {
+    const int* tc = hist.tok[(t - 1) & 1] + static_cast<long long>(hist.row_parent[r]) * T;
+    int* tn = hist.tok[t & 1] + static_cast<long long>(r) * T;
+    for (int j = threadIdx.x; j < t - 1; j += blockDim.x) tn[j] = tc[j];
+    if (threadIdx.x == 0 && t - 1 < T) tn[t - 1] = hist.row_prev[r];
+  }
+  for (int j = threadIdx.x; j <= t; j += blockDim.x) {
+    const int a = fold && j == t ? r : ar[j];
+    arow[j] = a;
+    if (fold && j < T) an[j] = a;
+    if (j < t && (early & 2))
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       cache + (static_cast<long long>(j) * r_max + a) * ld3 + d),
+                   "r"(static_cast<unsigned>(2 * d * sizeof(float)))
+                   : "memory");
+  }
+  if (early) pdl_wait();
+  pdl_trigger();
+  trace_begin(op.tr);
+  __syncthreads();
   for (int h = warp; h < heads; h += nw) {
     const float* q = cache + (static_cast<long long>(t) * r_max + r) * ld3 + h * dh;
     for (int c = lane; c < dh; c += 32) qs[c] = q[c];
@@ -1001,7 +1035,8 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
 void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const int* anc0,
                                const int* anc1, const int* d_rows, const int* d_step, int d,
                                int heads, float scale, float* ctx, long long ldc,
-                               const OperandOut& op, cudaStream_t st) {
+                               const OperandOut& op, cudaStream_t st, int early,
+                               const HistReorder& hist) {
   if (r_max <= 0) return;
   const int dh = d / heads;
   if (heads < 1 || heads * dh != d) fail(kUsageError, "attention: heads must divide d_model");
@@ -1009,8 +1044,16 @@ void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const i
   const size_t smem = sizeof(float) * (size_t(nw) * dec_attn_warp_floats(dh, T) + d + 33 + T);
   auto k = dh == 64 ? dec_self_attention_kernel<64> : dec_self_attention_kernel<0>;
   set_smem_limit(reinterpret_cast<const void*>(k), smem, "decoder self-attention");
+  // MTG_KV_PREFETCH=1: L2 prefetch of the cached keys / values before the
+  // wait (A/B; measured -0.8 % fp32 at batch 64: the prefetch competes with
+  // the QKV GEMM's L2 traffic).
+  static const bool prefetch = [] {
+    const char* e = std::getenv("MTG_KV_PREFETCH");
+    return e && e[0] == '1';
+  }();
+  const int mode = early ? (prefetch ? 3 : 1) : 0;
   launch_k(k, r_max, nw * 32, smem, st, qkv_cache, r_max, T, anc0, anc1, d_rows, d_step, d, dh,
-           scale, ctx, ldc, op);
+           scale, ctx, ldc, op, mode, hist);
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -28,6 +28,17 @@ struct OperandOut {
   KTrace tr;  // MTG_TRACE timeline slot of the kernel writing this operand
 };
 
+// Beam history reorder folded into the layer-0 decoder self-attention
+// (beam.cu beam_reorder_kernel): row r's ancestry / token tables of step t
+// from its parent's, written by the attention before its dependency wait.
+struct HistReorder {
+  int on = 0;
+  int* anc[2] = {nullptr, nullptr};
+  int* tok[2] = {nullptr, nullptr};
+  const int* row_parent = nullptr;
+  const int* row_prev = nullptr;
+};
+
 // Empty dependent kernel (148 CTAs): the PDL launch floor, for timing.
 void launch_noop(cudaStream_t st);
 
@@ -124,7 +135,8 @@ void launch_quantize_sent(const float* x, long long ldx, int rows, int n, const 
 void launch_dec_self_attention(const float* qkv_cache, int r_max, int T, const int* anc0,
                                const int* anc1, const int* d_rows, const int* d_step, int d,
                                int heads, float scale, float* ctx, long long ldc,
-                               const OperandOut& op, cudaStream_t st);
+                               const OperandOut& op, cudaStream_t st,
+                               int early = 1, const HistReorder& hist = {});
 
 // Decoder cross-attention: row r attends to its sentence's encoder rows
 // (enc_off[s]..+enc_len[s]) in ckv ([M_enc][2d] = [k | v]).

@@ -330,7 +330,9 @@ def test_step_fusion_modes_agree():
                 dict(MTG_FUSED_TAIL="0"), dict(MTG_LOGITS_PERSISTENT="1"),
                 dict(MTG_NO_SPLIT_K="1"), dict(MTG_ENC_GRAPH="0"), dict(MTG_NO_ENC_FUSION="1"),
                 dict(MTG_STEPS_PER_GRAPH="1"), dict(MTG_DEVICE_LOOP="0"),
-                dict(MTG_SPLIT_CTAS="148"), dict(MTG_MIN_BN="64"), dict(MTG_NO_PDL="1")]
+                dict(MTG_SPLIT_CTAS="148"), dict(MTG_MIN_BN="64"), dict(MTG_NO_PDL="1"),
+                dict(MTG_FOLD_REORDER="0"), dict(MTG_SPLITK_DIST="0"), dict(MTG_CLUSTER_CAP="0"),
+                dict(MTG_SMALL_BATCH="0")]
     for v in variants:  # every A/B switch must leave the bits unchanged
         env = dict(os.environ, **v)
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
