@@ -244,7 +244,7 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   // Just under one tile per SM at 32 columns (the fused QKV GEMM at batch 64:
   // 144 tiles, split 2): 64-column tiles split 3-4 ways read the activation
   // rows half as often (measured int8 5.2 -> 4.5 us, fp32 11.6 -> 11.2 us).
-  if (!force_bn && !ffn_up_deep && bn == 32 && p.m_tiles * ((n + 31) / 32) > 96 &&
+  if (!force_bn && !ffn_up_deep && bn == 32 && p.m_tiles >= 3 && p.m_tiles * ((n + 31) / 32) > 96 &&
       p.m_tiles * ((n + 31) / 32) < 148)
     bn = 64;
   p.bn = bn;

@@ -345,10 +345,13 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     const int N = ep.N;
     const long long ldc = ep.ldc, ldr = ep.ldr;
     float* const Cbase = ep.C + step_off + static_cast<long long>(rbase) * ldc;
-    // BN = 32 (the N = d_model residual GEMMs): each epilogue warp owns one
-    // 32-row x 16-column chunk, so its residual and bias are fetched while
-    // the MMAs are still running (measured slower for BN = 64).
-    constexpr bool kPrefetch = (BN == 32 && EPI != kEpiSoftmaxParts);
+    // BN = 32 (the N = d_model residual GEMMs) and the BN = 64 FFN-down
+    // (compile-time bias + residual): each epilogue warp owns one 32-row x
+    // BN/2-column chunk, so its residual and bias are fetched while the MMAs
+    // are still running (after the accumulator wait they cost a dependent L2
+    // round trip per 8 rows; without a residual, BN = 64 measured slower).
+    constexpr bool kPrefetch =
+        EPI != kEpiSoftmaxParts && (BN == 32 || (BN == 64 && FL >= 0 && (FL & 4) != 0));
     float res_pre[kPrefetch ? 32 : 1];
     float bias_pre = 0.0f;
     if constexpr (kPrefetch) {

@@ -30,8 +30,8 @@ struct KTrace {
   int slot = 0;
   int per_step = 0;
   const int* d_step = nullptr;
-  // MTG_TRACE=2: per-phase times (latest CTA to reach phase i), kTracePhases
-  // per (step, slot)
+  // MTG_TRACE=2 (MTG_TRACE_PHASES builds): per-phase times (latest CTA to
+  // reach phase i), kTracePhases per (step, slot)
   unsigned long long* ph = nullptr;
 };
 constexpr int kTracePhases = 8;
@@ -48,10 +48,17 @@ __device__ __forceinline__ void trace_end(const KTrace& k) {
   if (k.buf && threadIdx.x == 0)
     atomicMax(&k.buf[2 * (static_cast<long long>(*k.d_step) * k.per_step + k.slot) + 1], gtimer());
 }
+// Compiled in only for diagnostics builds (make EXTRA=-DMTG_TRACE_PHASES=1,
+// tools/build_phases.sh): even untaken, the checks cost ~0.1-0.4 us per GEMM.
+#ifndef MTG_TRACE_PHASES
+#define MTG_TRACE_PHASES 0
+#endif
 __device__ __forceinline__ void trace_phase(const KTrace& k, int i) {
-  if (k.ph)
-    atomicMax(&k.ph[(static_cast<long long>(*k.d_step) * k.per_step + k.slot) * kTracePhases + i],
-              gtimer());
+  if constexpr (MTG_TRACE_PHASES != 0) {
+    if (k.ph)
+      atomicMax(&k.ph[(static_cast<long long>(*k.d_step) * k.per_step + k.slot) * kTracePhases + i],
+                gtimer());
+  }
 }
 // Variants with the step passed in (kernels that advance the step counter).
 __device__ __forceinline__ void trace_begin_at(const KTrace& k, int t) {

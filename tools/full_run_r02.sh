@@ -1,4 +1,5 @@
-# Round-2 measurement run (tests, smoke, bench arms, in-graph timelines,
+# Round-2 measurement run (needs build_ab/libminimt_gpu_phases.so from
+# tools/build_phases.sh for the per-phase timelines) (tests, smoke, bench arms, in-graph timelines,
 # launch lists, ncu captures); outputs under gpurun_out/r02_*. Summaries are
 # copied into profiles/r02/ (tools/ncu_summary.py, tools/launches.py).
 set -x
@@ -12,7 +13,8 @@ python bench.py --steps 5 --warmup 3 --precision bf16 --no-cpu-baseline > $O/r02
 python bench.py --impl reference --steps 2 --warmup 1 --precision f32 > $O/r02_bench_ref_f32.json
 cat $O/r02_bench_*.json
 for p in f32 int8 bf16; do
-  MTG_TRACE=2 python tools/step_trace.py $p 64 > $O/r02_trace_${p}_b64.txt 2>&1
+  MTG_TRACE=1 python tools/step_trace.py $p 64 > $O/r02_trace_${p}_b64.txt 2>&1
+  MTG_LIB_PATH=build_ab/libminimt_gpu_phases.so MTG_TRACE=2 python tools/step_trace.py $p 64 > $O/r02_trace_phases_${p}_b64.txt 2>&1
   MTG_TRACE=1 python tools/b1_trace.py $p > $O/r02_trace_${p}_b1.txt 2>&1
 done
 # ncu cannot profile kernels inside graphs with conditional (while) nodes:
