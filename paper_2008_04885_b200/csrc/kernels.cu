@@ -677,14 +677,32 @@ __device__ __forceinline__ void stage_rows64(float* stage, int c0, int n, KP kp,
   cp_async_commit();
 }
 
+// Row j (stage row jr) alone, by lanes 0-15, as its own cp.async group.
+__device__ __forceinline__ void stage_row64(float* stage, int jr, const float* src, int lane) {
+  if (lane < 16) cp_async16(stage + jr * 64 + ((lane ^ (jr & 15)) << 2), src + 4 * lane);
+  cp_async_commit();
+}
+
+// L2 prefetch of rows c0 .. c0+31 (< n), 256 B each (lane = row).
+template <class VP>
+__device__ __forceinline__ void prefetch_rows64(int c0, int n, VP vp, int lane) {
+  if (c0 + lane < n)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(vp(c0 + lane)) : "memory");
+}
+
+// k0_staged: the caller already issued (committed) the copies of key chunk 0.
 template <class KP, class VP>
 __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, float scale, KP kp,
-                                                     VP vp, float* stage, float* s, float* out) {
+                                                     VP vp, float* stage, float* s, float* out,
+                                                     const KTrace* tr = nullptr,
+                                                     bool k0_staged = false) {
   const int lane = threadIdx.x & 31;
+  const bool ph = tr && lane == 0;
   float mx = kNegInf;
   for (int c0 = 0; c0 < n; c0 += 32) {
-    stage_rows64(stage, c0, n, kp, lane);
+    if (!(k0_staged && c0 == 0)) stage_rows64(stage, c0, n, kp, lane);
     cp_async_wait_warp();
+    if (ph && c0 == 0) trace_phase(*tr, 1);
     const int j = c0 + lane;
     if (j < n) {
       const float* kr = stage + lane * 64;
@@ -704,6 +722,7 @@ __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, floa
     }
     __syncwarp();
   }
+  if (ph) trace_phase(*tr, 2);
   stage_rows64(stage, 0, n, vp, lane);  // first value chunk overlaps the softmax
   mx = warp_allmax(mx);
   float part = 0.0f;
@@ -722,6 +741,7 @@ __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, floa
   for (int c0 = 0; c0 < n; c0 += 32) {
     if (c0 != 0) stage_rows64(stage, c0, n, vp, lane);
     cp_async_wait_warp();
+    if (ph && c0 == 0) trace_phase(*tr, 3);
     const int nk = min(32, n - c0);
     for (int jr = 0; jr < nk; ++jr) {
       const float p = s[c0 + jr];
@@ -733,6 +753,7 @@ __device__ __forceinline__ void attend_warp_staged64(const float* q, int n, floa
   }
   out[lane] = acc_a;
   out[32 + lane] = acc_b;
+  if (ph) trace_phase(*tr, 4);
   __syncwarp();
 }
 
@@ -807,24 +828,44 @@ __global__ void __launch_bounds__(256, 3)
                    "r"(static_cast<unsigned>(2 * d * sizeof(float)))
                    : "memory");
   }
+  __syncthreads();  // ancestry rows visible to every warp
+  // Early (DH = 64): the first head's cached keys of chunk 0 (positions < t,
+  // written in earlier steps) are copied now and its values prefetched into
+  // L2; after the wait only the query and position t's key follow.
+  const bool pre = DH == 64 && early && warp < heads;
+  auto kp_of = [&](int h) {
+    const float* kb = cache + d + h * dh;
+    return [=](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; };
+  };
+  if (pre) {
+    stage_rows64(stage, 0, min(t, 32), kp_of(warp), lane);
+    const float* vb = cache + 2 * d + warp * dh;
+    prefetch_rows64(
+        0, min(t, 32),
+        [=](int j) { return vb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; }, lane);
+  }
   if (early) pdl_wait();
   pdl_trigger();
   trace_begin(op.tr);
-  __syncthreads();
+  if (threadIdx.x == 0) trace_phase(op.tr, 0);
   for (int h = warp; h < heads; h += nw) {
     const float* q = cache + (static_cast<long long>(t) * r_max + r) * ld3 + h * dh;
-    for (int c = lane; c < dh; c += 32) qs[c] = q[c];
-    __syncwarp();
     const float* kb = cache + d + h * dh;
     auto kp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3; };
     auto vp = [&](int j) { return kb + (static_cast<long long>(j) * r_max + arow[j]) * ld3 + d; };
+    const bool k0 = pre && h == warp;
+    if (k0 && t < 32) stage_row64(stage, t, kp(t), lane);  // this step's key (the QKV GEMM's)
+    for (int c = lane; c < dh; c += 32) qs[c] = q[c];
+    __syncwarp();
     if constexpr (DH == 64)
-      attend_warp_staged64(qs, t + 1, scale, kp, vp, stage, ss, row + h * dh);
+      attend_warp_staged64(qs, t + 1, scale, kp, vp, stage, ss, row + h * dh,
+                           h == 0 ? &op.tr : nullptr, k0);
     else
       attend_warp<DH>(qs, t + 1, dh, scale, kp, vp, ss, row + h * dh);
     __syncwarp();
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_phase(op.tr, 5);
   finish_ctx_row(row, d, r, ctx, ldc, op, red);
   trace_end(op.tr);
 }
@@ -837,31 +878,48 @@ __global__ void __launch_bounds__(256, 3)
                                const int* __restrict__ enc_off, const int* __restrict__ enc_len,
                                const int* d_rows, int max_src, int d, int dh_rt, float scale,
                                float* __restrict__ ctx, long long ldc, OperandOut op) {
-  pdl_wait();
-  pdl_trigger();
-  trace_begin(op.tr);
   extern __shared__ __align__(16) float sm[];
   const int r = blockIdx.x;
-  if (r >= *d_rows) return;
+  // Before the dependency wait: the row's sentence (beam state of the
+  // previous step's tail) and, for the first head, the copies of the
+  // encoder keys of chunk 0 plus an L2 prefetch of its values; after the
+  // wait only the query (the cross-Wq GEMM's output).
+  const int R = *d_rows;
+  if (r >= R) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
   const int dh = DH > 0 ? DH : dh_rt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int heads = d / dh;
   const int s = row_sent[r];
   const int n = enc_len[s];
+  const long long off = static_cast<long long>(enc_off[s]) * 2 * d;
   const int W = dec_attn_warp_floats(DH > 0 ? DH : dh, max_src);
   float* stage = sm + warp * W;
   float* qs = stage + (DH == 64 ? kStageFloats : 0);
   float* ss = qs + round4(dh);
   float* row = sm + nw * W;
   float* red = row + d;
+  const bool pre = DH == 64 && warp < heads;
+  if (pre) {
+    const float* kv = ckv + off + warp * dh;
+    stage_rows64(stage, 0, n, [=](int j) { return kv + static_cast<long long>(j) * 2 * d; }, lane);
+    prefetch_rows64(0, n, [=](int j) { return kv + static_cast<long long>(j) * 2 * d + d; }, lane);
+  }
+  pdl_wait();
+  pdl_trigger();
+  trace_begin(op.tr);
   for (int h = warp; h < heads; h += nw) {
-    const float* kv = ckv + static_cast<long long>(enc_off[s]) * 2 * d + h * dh;
+    const float* kv = ckv + off + h * dh;
     for (int c = lane; c < dh; c += 32) qs[c] = cq[r * ldq + h * dh + c];
     __syncwarp();
     auto kp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d; };
     auto vp = [&](int j) { return kv + static_cast<long long>(j) * 2 * d + d; };
     if constexpr (DH == 64)
-      attend_warp_staged64(qs, n, scale, kp, vp, stage, ss, row + h * dh);
+      attend_warp_staged64(qs, n, scale, kp, vp, stage, ss, row + h * dh, nullptr,
+                           pre && h == warp);
     else
       attend_warp<DH>(qs, n, dh, scale, kp, vp, ss, row + h * dh);
     __syncwarp();
