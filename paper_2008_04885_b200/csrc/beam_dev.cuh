@@ -207,7 +207,7 @@ __device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, 
 // scans the live counts, writes the compacted rows and advances the step.
 // live_s / row0_s: [N] shared ints; is_last: one shared int.
 __device__ __forceinline__ void finish_select(const BeamDev& b, int t, int* live_s, int* row0_s,
-                                              int* is_last) {
+                                              int* is_last, const KTrace* tr = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Last-CTA election: every CTA's writes are made visible before its ticket.
   // A single-CTA grid (batch-1) is its own last CTA: the block barrier makes
@@ -222,6 +222,7 @@ __device__ __forceinline__ void finish_select(const BeamDev& b, int t, int* live
     if (!*is_last) return;
     __threadfence();
   }
+  if (tr && threadIdx.x == 0) trace_phase_at(*tr, t, 3);
   for (int s = threadIdx.x; s < b.N; s += blockDim.x) live_s[s] = __ldcg(b.sent_live + s);
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the live counts (32 sentences per pass)
@@ -277,6 +278,7 @@ __device__ __forceinline__ void finish_select(const BeamDev& b, int t, int* live
   if (threadIdx.x == 0) {
     *b.step = t + 1;
     *b.sel_count = 0;
+    if (tr) trace_phase_at(*tr, t, 4);
   }
 }
 

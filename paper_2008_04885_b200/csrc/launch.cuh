@@ -60,6 +60,12 @@ __device__ __forceinline__ void trace_phase(const KTrace& k, int i) {
                 gtimer());
   }
 }
+__device__ __forceinline__ void trace_phase_at(const KTrace& k, int t, int i) {
+  if constexpr (MTG_TRACE_PHASES != 0) {
+    if (k.ph)
+      atomicMax(&k.ph[(static_cast<long long>(t) * k.per_step + k.slot) * kTracePhases + i], gtimer());
+  }
+}
 // Variants with the step passed in (kernels that advance the step counter).
 __device__ __forceinline__ void trace_begin_at(const KTrace& k, int t) {
   if (k.buf && threadIdx.x == 0)

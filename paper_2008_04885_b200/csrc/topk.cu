@@ -82,13 +82,39 @@ __device__ __forceinline__ void block_best(float& bs, int& bt, float* rf, int* r
   grp_sync(bar);
 }
 
+// Bitonic sort of one (score, token) pair per lane across the warp, best
+// first in the (score desc, token asc) order; empty entries (token INT_MAX)
+// sort last. Lane k ends with the k-th best.
+__device__ __forceinline__ void warp_sort_best_first(float& s, int& t, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, s, j);
+      const int ot = __shfl_xor_sync(0xffffffffu, t, j);
+      const bool o_better =
+          ot != INT_MAX && (t == INT_MAX || better2(os, ot, s, t));
+      const bool keep_better = ((lane & k) == 0) == ((lane & j) == 0);
+      if (keep_better ? o_better : (!o_better && ot != t)) {
+        s = os;
+        t = ot;
+      }
+    }
+  }
+}
+
 // Per-group shared scratch of the row routines: CAP ints of rescan list
 // (merge, kMaxSoftmaxSlices) or shortlist logits (kMaxShortlist).
+constexpr int kSurvCap = 128;  // rescanned elements at or above the threshold
+
 template <int CAP>
 struct RowScratchT {
   float red_f[kMT / 32];
   int red_i[kMT / 32];
   int n_list;
+  int n_surv;
+  float surv_s[kSurvCap];
+  int surv_t[kSurvCap];
   int list[CAP];
 };
 using MergeScratch = RowScratchT<kMaxSoftmaxSlices>;
@@ -102,7 +128,7 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
                                       const float* __restrict__ part_s,
                                       const int* __restrict__ part_arg, long long part_ld,
                                       int nsub, const BeamDev& b, int tid, int bar,
-                                      MergeScratch& sc_) {
+                                      MergeScratch& sc_, const KTrace* tr = nullptr, int t = 0) {
   float* red_f = sc_.red_f;
   int* red_i = sc_.red_i;
   int* list_s = sc_.list;
@@ -115,7 +141,10 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
   const int* pa = part_arg + r * part_ld;
   const float* x = logits + r * ldl;
   const float plp = b.row_lp[r];
-  if (tid == 0) n_list_s = 0;
+  if (tid == 0) {
+    n_list_s = 0;
+    sc_.n_surv = 0;
+  }
 
   // All partial loads first (one L2 round trip), then the math.
   float mv[kSubPerThread], sv[kSubPerThread];
@@ -151,6 +180,7 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
   const float total = __fadd_rn(__fadd_rn(red_f[0], red_f[1]), __fadd_rn(red_f[2], red_f[3]));
   grp_sync(bar);
   const float lse = __fadd_rn(det_logf(total), M);
+  if (tr && tid == 0) trace_phase_at(*tr, t, 5);
 
   // Slice-max scores; a slice with no max (all NaN / empty) never competes.
   float sc[kSubPerThread];
@@ -159,29 +189,42 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
     sc[i] = __fadd_rn(plp, __fsub_rn(mv[i], lse));
     if (sc[i] != sc[i]) at[i] = -1;
   }
-  // kB-th best slice max: kB rounds, each taking the best entry ranked
-  // strictly below the previous pick.
-  float last_s = kPosInf, thr = kNegInf;
-  int last_t = -1;
-  for (int k = 0; k < kB; ++k) {
+  // Rescan threshold T <= the kB-th best slice maximum (exactness needs no
+  // more): every warp sorts its 32 threads' best slice maxima and offers its
+  // kB-th; T = the best offer. That warp has kB slice maxima at or above T,
+  // so the kB-th best slice maximum is too, and the rescan set (slices whose
+  // maximum scores >= T) holds every top-kB element. No offer (fewer than kB
+  // valid slices in every warp): every valid slice is rescanned.
+  float thr = kNegInf;
+  {
+    float ts = kNegInf;
+    int tt = INT_MAX;
+#pragma unroll
+    for (int i = 0; i < kSubPerThread; ++i)
+      if (at[i] >= 0 && (tt == INT_MAX || better2(sc[i], at[i], ts, tt))) {
+        ts = sc[i];
+        tt = at[i];
+      }
+    warp_sort_best_first(ts, tt, lane);
+    const float ws = __shfl_sync(0xffffffffu, ts, kB - 1);
+    const int wt = __shfl_sync(0xffffffffu, tt, kB - 1);
+    if (lane == 0) {
+      red_f[warp] = ws;
+      red_i[warp] = wt;
+    }
+    grp_sync(bar);
     float bs = kNegInf;
     int bt = INT_MAX;
 #pragma unroll
-    for (int i = 0; i < kSubPerThread; ++i)
-      if (at[i] >= 0 && better2(last_s, last_t, sc[i], at[i]) &&
-          (bt == INT_MAX || better2(sc[i], at[i], bs, bt))) {
-        bs = sc[i];
-        bt = at[i];
+    for (int w = 0; w < kMT / 32; ++w)
+      if (red_i[w] != INT_MAX && (bt == INT_MAX || better2(red_f[w], red_i[w], bs, bt))) {
+        bs = red_f[w];
+        bt = red_i[w];
       }
-    block_best(bs, bt, red_f, red_i, tid, bar);
-    if (bt == INT_MAX) {  // fewer than kB slices: every valid slice is rescanned
-      thr = kNegInf;
-      break;
-    }
-    last_s = bs;
-    last_t = bt;
-    thr = bs;
+    grp_sync(bar);
+    if (bt != INT_MAX) thr = bs;
   }
+  if (tr && tid == 0) trace_phase_at(*tr, t, 6);
   // Slices to rescan: score(m_k) >= thr (normally exactly kB of them).
 #pragma unroll
   for (int i = 0; i < kSubPerThread; ++i)
@@ -202,39 +245,88 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
 #pragma unroll
   for (int e = 0; e < kCache; ++e)
     cs[e] = cc[e] < V ? __fadd_rn(plp, __fsub_rn(cs[e], lse)) : kNegInf;
-  last_s = kPosInf;
-  last_t = -1;
-  for (int k = 0; k < kB; ++k) {
-    float bs = kNegInf;
-    int bt = INT_MAX;
+  // Survivors: rescanned elements scoring >= T (at least kB of them: the
+  // kB slice maxima at or above T). Their rank in (score desc, token asc)
+  // order is their candidate slot.
+  int* n_surv_s = &sc_.n_surv;
 #pragma unroll
-    for (int e = 0; e < kCache; ++e) {
-      const int col = cc[e];
-      if (col < V && cs[e] == cs[e] && better2(last_s, last_t, cs[e], col) &&
-          (bt == INT_MAX || better2(cs[e], col, bs, bt))) {
-        bs = cs[e];
-        bt = col;
+  for (int e = 0; e < kCache; ++e) {
+    const int col = cc[e];
+    if (col < V && cs[e] == cs[e] && cs[e] >= thr) {
+      const int at_ = atomicAdd(n_surv_s, 1);
+      if (at_ < kSurvCap) {
+        sc_.surv_s[at_] = cs[e];
+        sc_.surv_t[at_] = col;
       }
     }
-    for (int idx = warp + kW * kCache; idx < n_list; idx += kW) {  // long lists (ties)
-      const int col = list_s[idx] * 32 + lane;
-      if (col < V) {
-        const float s = __fadd_rn(plp, __fsub_rn(x[col], lse));
-        if (s == s && better2(last_s, last_t, s, col) && (bt == INT_MAX || better2(s, col, bs, bt))) {
-          bs = s;
-          bt = col;
+  }
+  for (int idx = warp + kW * kCache; idx < n_list; idx += kW) {  // long lists (ties)
+    const int col = list_s[idx] * 32 + lane;
+    if (col < V) {
+      const float sv = __fadd_rn(plp, __fsub_rn(x[col], lse));
+      if (sv == sv && sv >= thr) {
+        const int at_ = atomicAdd(n_surv_s, 1);
+        if (at_ < kSurvCap) {
+          sc_.surv_s[at_] = sv;
+          sc_.surv_t[at_] = col;
         }
       }
     }
-    block_best(bs, bt, red_f, red_i, tid, bar);
-    if (tid == 0) {
-      b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
-      b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
-    }
-    if (bt == INT_MAX) break;
-    last_s = bs;
-    last_t = bt;
   }
+  grp_sync(bar);
+  const int n_surv = *n_surv_s;
+  if (n_surv <= kSurvCap) {
+    for (int i = tid; i < n_surv; i += kMT) {
+      const float si = sc_.surv_s[i];
+      const int ti = sc_.surv_t[i];
+      int rank = 0;
+      for (int j = 0; j < n_surv; ++j) rank += better2(sc_.surv_s[j], sc_.surv_t[j], si, ti);
+      if (rank < kB) {
+        b.cand_score[static_cast<long long>(r) * b.B + rank] = si;
+        b.cand_tok[static_cast<long long>(r) * b.B + rank] = ti;
+      }
+    }
+    for (int k = n_surv + tid; k < kB; k += kMT) {  // fewer valid elements than kB
+      b.cand_score[static_cast<long long>(r) * b.B + k] = kNegInf;
+      b.cand_tok[static_cast<long long>(r) * b.B + k] = INT_MAX;
+    }
+  } else {
+    // Many ties at T (degenerate logits): kB group-wide argmax rounds.
+    float last_s = kPosInf;
+    int last_t = -1;
+    for (int k = 0; k < kB; ++k) {
+      float bs = kNegInf;
+      int bt = INT_MAX;
+#pragma unroll
+      for (int e = 0; e < kCache; ++e) {
+        const int col = cc[e];
+        if (col < V && cs[e] == cs[e] && better2(last_s, last_t, cs[e], col) &&
+            (bt == INT_MAX || better2(cs[e], col, bs, bt))) {
+          bs = cs[e];
+          bt = col;
+        }
+      }
+      for (int idx = warp + kW * kCache; idx < n_list; idx += kW) {  // long lists (ties)
+        const int col = list_s[idx] * 32 + lane;
+        if (col < V) {
+          const float s = __fadd_rn(plp, __fsub_rn(x[col], lse));
+          if (s == s && better2(last_s, last_t, s, col) && (bt == INT_MAX || better2(s, col, bs, bt))) {
+            bs = s;
+            bt = col;
+          }
+        }
+      }
+      block_best(bs, bt, red_f, red_i, tid, bar);
+      if (tid == 0) {
+        b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
+        b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
+      }
+      if (bt == INT_MAX) break;
+      last_s = bs;
+      last_t = bt;
+    }
+  }
+  if (tr && tid == 0) trace_phase_at(*tr, t, 7);
   // Rows with fewer than kB candidates leave the rest invalid.
   for (int k = kB + tid; k < b.B; k += kMT) {
     b.cand_score[static_cast<long long>(r) * b.B + k] = kNegInf;
@@ -437,19 +529,22 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   const int s = blockIdx.x;
   const int t = *b.step;
   trace_begin_at(b.tr_a, t);
+  if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 0);
   if (!b.sent_done[s]) {
     const int L = b.sent_live[s], r0 = b.sent_row0[s];
     for (int i = g; i < L; i += G) {
       if constexpr (MODE == 0)
         merge_row(r0 + i, ta.logits, ta.ldl, ta.part_m, ta.part_s, ta.part_arg, ta.part_ld,
-                  ta.nsub, b, tid, 1 + g, scr[g]);
+                  ta.nsub, b, tid, 1 + g, scr[g], g == 0 ? &b.tr_a : nullptr, t);
       else
         shortlist_row<MODE - 1>(r0 + i, sa, b, tid, 1 + g, scr[g]);
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 1);
   if (threadIdx.x < 32) select_sentence(b, s, t, threadIdx.x);
-  finish_select(b, t, live_s, row0_s, &is_last);
+  if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 2);
+  finish_select(b, t, live_s, row0_s, &is_last, &b.tr_a);
   trace_end_at(b.tr_a, t);
 }
 
