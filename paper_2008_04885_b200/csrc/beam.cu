@@ -48,17 +48,22 @@ constexpr int kSelWarps = 4;
 // Warp per sentence across the grid; the last CTA to finish (atomic ticket)
 // computes the row offsets and writes the compacted rows.
 __global__ void __launch_bounds__(kSelWarps * 32) beam_select_kernel(BeamDev b) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ int sel_smem[];  // [N] new live counts, [N] first rows
   int* live_s = sel_smem;
   int* row0_s = sel_smem + b.N;
   __shared__ int is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // The first sentence's beam state (the previous step tail's) is loaded
+  // before the dependency wait.
+  const int s0 = blockIdx.x * nwarps + warp;
+  SentState st0{};
+  if (s0 < b.N) st0 = load_sent_state(b, s0);
+  pdl_wait();
+  pdl_trigger();
   const int t = *b.step;
   trace_begin_at(b.tr_b, t);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int s = blockIdx.x * nwarps + warp; s < b.N; s += gridDim.x * nwarps)
-    select_sentence(b, s, t, lane);
+  for (int s = s0; s < b.N; s += gridDim.x * nwarps)
+    select_sentence(b, s, t, lane, s == s0 ? st0 : load_sent_state(b, s));
   finish_select(b, t, live_s, row0_s, &is_last);
   trace_end_at(b.tr_b, t);
 }

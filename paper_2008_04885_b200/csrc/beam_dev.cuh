@@ -24,18 +24,37 @@ __device__ __forceinline__ bool better3(float a, int pa, int ta, float b, int pb
   return ta < tb;
 }
 
-// One warp: candidates of sentence s (cand_score / cand_tok of its live rows)
-// -> sel_* (surviving hypotheses), finished-list update, termination and
-// the sentence result; writes sent_live[s].
-__device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, int lane) {
+// Per-sentence beam state, loaded together (one round trip). It is written
+// only by the step tail, so a tail kernel may load it before its dependency
+// wait.
+struct SentState {
+  int done, L, r0, maxlen, has, blen;
+  float bnorm, blp;
+};
+__device__ __forceinline__ SentState load_sent_state(const BeamDev& b, int s) {
+  SentState st;
+  st.done = b.sent_done[s];
+  st.L = b.sent_live[s];
+  st.r0 = b.sent_row0[s];
+  st.maxlen = b.sent_maxlen[s];
+  st.has = b.best_has[s];
+  st.blen = b.best_len[s];
+  st.bnorm = b.best_norm[s];
+  st.blp = b.best_lp[s];
+  return st;
+}
+
+// Sequential form (kB selection rounds of warp argmax), for sentences with
+// more than 32 candidates (beam * beam > 32).
+__device__ __forceinline__ void select_sentence_seq(const BeamDev& b, int s, int t, int lane,
+                                                    const SentState& st) {
   const int kB = min(b.B, b.V);
   const int T = b.T;
   const int* tok_cur = b.tok[t & 1];
-  // Per-sentence state, loaded together (one round trip).
-  const int done = b.sent_done[s], L = b.sent_live[s], r0 = b.sent_row0[s];
-  const int maxlen = b.sent_maxlen[s];
-  int has = b.best_has[s], blen = b.best_len[s];
-  float bnorm = b.best_norm[s], blp = b.best_lp[s];
+  const int done = st.done, L = st.L, r0 = st.r0;
+  const int maxlen = st.maxlen;
+  int has = st.has, blen = st.blen;
+  float bnorm = st.bnorm, blp = st.blp;
   if (done) return;
   const int nc = L * kB;
   // Candidates of this sentence, loaded once: lane owns c = lane + 32 i.
@@ -183,6 +202,161 @@ __device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, 
       const int pr = __shfl_sync(0xffffffffu, my_parent, bq);
       const int tk = __shfl_sync(0xffffffffu, my_tok, bq);
       const float lpq = __shfl_sync(0xffffffffu, my_lp, bq);
+      for (int j = lane; j < t; j += 32)
+        b.res_tok[static_cast<long long>(s) * T + j] = tok_cur[static_cast<long long>(pr) * T + j];
+      if (lane == 0) {
+        b.res_tok[static_cast<long long>(s) * T + t] = tk;
+        b.res_len[s] = t + 1;
+        b.res_lp[s] = lpq;
+        b.res_norm[s] = bn;
+        b.res_flags[s] = 2u;
+      }
+    }
+    if (lane == 0) {
+      b.res_status[s] = 0;
+      b.sent_done[s] = 1;
+    }
+    new_live = 0;
+  }
+  if (lane == 0) b.sent_live[s] = new_live;
+  __syncwarp();
+}
+
+// One warp: candidates of sentence s (cand_score / cand_tok of its live rows,
+// or cs_sm / ct_sm in shared memory at [row of the sentence * B + slot])
+// -> sel_* (surviving hypotheses), finished-list update, termination and the
+// sentence result; writes sent_live[s]. decode.cpp:55-109 with the stable
+// sort of the candidates replaced by ranks in the same total order
+// (score desc, parent asc, token asc): lane c holds candidate c and counts
+// the candidates ranked above it, so the kB-way selection needs no
+// sequential argmax rounds. Of the selected EOS candidates only the best
+// ranked can update the finished best (its normalised score is the largest
+// of this step's, and later ones only replace it on a strictly larger one).
+__device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, int lane,
+                                                const SentState& st,
+                                                const float* cs_sm = nullptr,
+                                                const int* ct_sm = nullptr) {
+  const int kB = min(b.B, b.V);
+  if (st.done) return;
+  const int nc = st.L * kB;
+  if (nc > 32) {
+    select_sentence_seq(b, s, t, lane, st);
+    return;
+  }
+  const int T = b.T;
+  const int* tok_cur = b.tok[t & 1];
+  const int r0 = st.r0;
+  float cs = kNegInf;
+  int cp = INT_MAX, ct = INT_MAX;
+  if (lane < nc) {
+    const int p = lane / kB, e = lane - p * kB;
+    cs = cs_sm ? cs_sm[p * b.B + e] : b.cand_score[static_cast<long long>(r0 + p) * b.B + e];
+    ct = ct_sm ? ct_sm[p * b.B + e] : b.cand_tok[static_cast<long long>(r0 + p) * b.B + e];
+    cp = p;
+  }
+  // no candidate (NaN logits) never competes
+  const bool valid = lane < nc && ct >= 0 && ct < b.V && cs == cs;
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  const int n_valid = __popc(vmask);
+  if (n_valid == 0) {  // invalid logits for this sentence: fail it (ValueError)
+    if (lane == 0) {
+      b.res_status[s] = 2;
+      b.res_flags[s] = 4u;
+      b.res_len[s] = 0;
+      b.sent_done[s] = 1;
+      b.sent_live[s] = 0;
+    }
+    __syncwarp();
+    return;
+  }
+  // decode.cpp:71: take min(|cands|, beam)
+  const int n_sel = min(b.B, n_valid);
+  int rank = 0, eos_above = 0;
+  for (int j = 0; j < nc; ++j) {
+    const float sj = __shfl_sync(0xffffffffu, cs, j);
+    const int pj = __shfl_sync(0xffffffffu, cp, j);
+    const int tj = __shfl_sync(0xffffffffu, ct, j);
+    if (((vmask >> j) & 1u) && better3(sj, pj, tj, cs, cp, ct)) {
+      ++rank;
+      eos_above += tj == kEosIdDev;
+    }
+  }
+  const bool sel = valid && rank < n_sel;
+  const bool eos = sel && ct == kEosIdDev;
+  // decode.cpp:77-80 + first max of normalized_score over finished
+  const unsigned first_eos = __ballot_sync(0xffffffffu, eos && eos_above == 0);
+  int has = st.has, blen = st.blen;
+  float bnorm = st.bnorm, blp = st.blp;
+  if (first_eos) {
+    const int src = __ffs(first_eos) - 1;
+    const float bs = __shfl_sync(0xffffffffu, cs, src);
+    const int pr = r0 + __shfl_sync(0xffffffffu, cp, src);
+    const float len = static_cast<float>(t) + 1.0f;
+    const float norm = __fdiv_rn(bs, det_powf(__fdiv_rn(__fadd_rn(5.0f, len), 6.0f), b.alpha));
+    if (!has || norm > bnorm) {
+      for (int j = lane; j < t; j += 32)
+        b.best_tok[static_cast<long long>(s) * T + j] = tok_cur[static_cast<long long>(pr) * T + j];
+      has = 1;
+      bnorm = norm;
+      blp = bs;
+      blen = t;
+      if (lane == 0) {
+        b.best_has[s] = 1;
+        b.best_norm[s] = norm;
+        b.best_lp[s] = bs;
+        b.best_len[s] = t;
+      }
+    }
+  }
+  // Surviving selections in rank order: slot q = rank - EOS ranked above.
+  const bool keep = sel && !eos;
+  const int q = keep ? rank - eos_above : INT_MAX;
+  if (keep) {
+    b.sel_parent[s * b.B + q] = r0 + cp;
+    b.sel_tok[s * b.B + q] = ct;
+    b.sel_lp[s * b.B + q] = cs;
+  }
+  int new_live = __popc(__ballot_sync(0xffffffffu, keep));
+  const int maxlen = st.maxlen;
+  if (new_live > 0 && t + 1 >= b.max_seq_len && maxlen > b.max_seq_len) {
+    // decode_step would be called past max_seq_len (model.cpp:618-619).
+    if (lane == 0) {
+      b.res_status[s] = 2;  // ValueError
+      b.res_flags[s] = 4u;
+      b.res_len[s] = 0;
+      b.sent_done[s] = 1;
+    }
+    new_live = 0;
+  } else if (new_live == 0 || t + 1 >= maxlen) {
+    if (has) {  // decode.cpp:89-98
+      for (int j = lane; j < blen; j += 32)
+        b.res_tok[static_cast<long long>(s) * T + j] = b.best_tok[static_cast<long long>(s) * T + j];
+      if (lane == 0) {
+        b.res_len[s] = blen;
+        b.res_lp[s] = blp;
+        b.res_norm[s] = bnorm;
+        b.res_flags[s] = 1u;
+      }
+    } else {  // decode.cpp:99-108: first max over live, truncated
+      const float len = static_cast<float>(t + 1) + 1.0f;
+      const float den = det_powf(__fdiv_rn(__fadd_rn(5.0f, len), 6.0f), b.alpha);
+      // First max of lp / den over the survivors (lowest slot q on ties).
+      float bn = keep ? __fdiv_rn(cs, den) : kNegInf;
+      int bq = q, bl = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float on = __shfl_xor_sync(0xffffffffu, bn, o);
+        const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (oq != INT_MAX && (bq == INT_MAX || on > bn || (on == bn && oq < bq))) {
+          bn = on;
+          bq = oq;
+          bl = ol;
+        }
+      }
+      const int pr = r0 + __shfl_sync(0xffffffffu, cp, bl);
+      const int tk = __shfl_sync(0xffffffffu, ct, bl);
+      const float lpq = __shfl_sync(0xffffffffu, cs, bl);
       for (int j = lane; j < t; j += 32)
         b.res_tok[static_cast<long long>(s) * T + j] = tok_cur[static_cast<long long>(pr) * T + j];
       if (lane == 0) {

@@ -128,7 +128,18 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
                                       const float* __restrict__ part_s,
                                       const int* __restrict__ part_arg, long long part_ld,
                                       int nsub, const BeamDev& b, int tid, int bar,
-                                      MergeScratch& sc_, const KTrace* tr = nullptr, int t = 0) {
+                                      MergeScratch& sc_, const KTrace* tr = nullptr, int t = 0,
+                                      float* cs_sm = nullptr, int* ct_sm = nullptr) {
+  // Candidate slot k of this row: shared memory (fused tail) or global.
+  auto put = [&](int k, float score, int tok) {
+    if (cs_sm) {
+      cs_sm[k] = score;
+      ct_sm[k] = tok;
+    } else {
+      b.cand_score[static_cast<long long>(r) * b.B + k] = score;
+      b.cand_tok[static_cast<long long>(r) * b.B + k] = tok;
+    }
+  };
   float* red_f = sc_.red_f;
   int* red_i = sc_.red_i;
   int* list_s = sc_.list;
@@ -281,15 +292,9 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
       const int ti = sc_.surv_t[i];
       int rank = 0;
       for (int j = 0; j < n_surv; ++j) rank += better2(sc_.surv_s[j], sc_.surv_t[j], si, ti);
-      if (rank < kB) {
-        b.cand_score[static_cast<long long>(r) * b.B + rank] = si;
-        b.cand_tok[static_cast<long long>(r) * b.B + rank] = ti;
-      }
+      if (rank < kB) put(rank, si, ti);
     }
-    for (int k = n_surv + tid; k < kB; k += kMT) {  // fewer valid elements than kB
-      b.cand_score[static_cast<long long>(r) * b.B + k] = kNegInf;
-      b.cand_tok[static_cast<long long>(r) * b.B + k] = INT_MAX;
-    }
+    for (int k = n_surv + tid; k < kB; k += kMT) put(k, kNegInf, INT_MAX);  // fewer valid elements than kB
   } else {
     // Many ties at T (degenerate logits): kB group-wide argmax rounds.
     float last_s = kPosInf;
@@ -318,8 +323,8 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
       }
       block_best(bs, bt, red_f, red_i, tid, bar);
       if (tid == 0) {
-        b.cand_score[static_cast<long long>(r) * b.B + k] = bt == INT_MAX ? kNegInf : bs;
-        b.cand_tok[static_cast<long long>(r) * b.B + k] = bt;
+        for (int kk = k; kk < (bt == INT_MAX ? kB : k + 1); ++kk)  // the rest invalid too
+          put(kk, bt == INT_MAX ? kNegInf : bs, bt);
       }
       if (bt == INT_MAX) break;
       last_s = bs;
@@ -327,11 +332,8 @@ __device__ __forceinline__ void merge_row(int r, const float* __restrict__ logit
     }
   }
   if (tr && tid == 0) trace_phase_at(*tr, t, 7);
-  // Rows with fewer than kB candidates leave the rest invalid.
-  for (int k = kB + tid; k < b.B; k += kMT) {
-    b.cand_score[static_cast<long long>(r) * b.B + k] = kNegInf;
-    b.cand_tok[static_cast<long long>(r) * b.B + k] = INT_MAX;
-  }
+  // Slots past kB (a vocabulary smaller than the beam) are invalid.
+  for (int k = kB + tid; k < b.B; k += kMT) put(k, kNegInf, INT_MAX);
 }
 
 __global__ void __launch_bounds__(kMT)
@@ -517,32 +519,45 @@ struct TailArgs {
 template <int MODE>  // 0 full vocabulary; 1..3 shortlist with PREC = MODE - 1
 __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, ShortlistArgs sa,
                                                            BeamDev b) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ __align__(16) unsigned char tail_smem[];
   const int G = blockDim.x / kMT, g = threadIdx.x / kMT, tid = threadIdx.x % kMT;
   using Scratch = std::conditional_t<MODE == 0, MergeScratch, ShortlistScratch>;
   Scratch* scr = reinterpret_cast<Scratch*>(tail_smem);
   int* live_s = reinterpret_cast<int*>(scr + G);
   int* row0_s = live_s + b.N;
+  float* cs_sm = reinterpret_cast<float*>(row0_s + b.N);  // [B rows][B slots]
+  int* ct_sm = reinterpret_cast<int*>(cs_sm + kMaxBeam * kMaxBeam);
   __shared__ int is_last;
+  __shared__ SentState st_s;
   const int s = blockIdx.x;
+  // The sentence's beam state is the previous step tail's: loaded before the
+  // dependency wait.
+  if (threadIdx.x == 0) st_s = load_sent_state(b, s);
+  pdl_wait();
+  pdl_trigger();
   const int t = *b.step;
   trace_begin_at(b.tr_a, t);
   if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 0);
-  if (!b.sent_done[s]) {
-    const int L = b.sent_live[s], r0 = b.sent_row0[s];
-    for (int i = g; i < L; i += G) {
+  __syncthreads();
+  const SentState st = st_s;
+  if (!st.done) {
+    for (int i = g; i < st.L; i += G) {
       if constexpr (MODE == 0)
-        merge_row(r0 + i, ta.logits, ta.ldl, ta.part_m, ta.part_s, ta.part_arg, ta.part_ld,
-                  ta.nsub, b, tid, 1 + g, scr[g], g == 0 ? &b.tr_a : nullptr, t);
+        merge_row(st.r0 + i, ta.logits, ta.ldl, ta.part_m, ta.part_s, ta.part_arg, ta.part_ld,
+                  ta.nsub, b, tid, 1 + g, scr[g], g == 0 ? &b.tr_a : nullptr, t,
+                  cs_sm + i * b.B, ct_sm + i * b.B);
       else
-        shortlist_row<MODE - 1>(r0 + i, sa, b, tid, 1 + g, scr[g]);
+        shortlist_row<MODE - 1>(st.r0 + i, sa, b, tid, 1 + g, scr[g]);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 1);
-  if (threadIdx.x < 32) select_sentence(b, s, t, threadIdx.x);
+  if (threadIdx.x < 32) {
+    if constexpr (MODE == 0)
+      select_sentence(b, s, t, threadIdx.x, st, cs_sm, ct_sm);
+    else
+      select_sentence(b, s, t, threadIdx.x, st);
+  }
   if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 2);
   finish_select(b, t, live_s, row0_s, &is_last, &b.tr_a);
   trace_end_at(b.tr_a, t);
@@ -566,7 +581,8 @@ void launch_topk_select(const float* logits, long long ldl, const float* part_m,
     fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
   const int G = std::min(b.B, 8);
   const size_t smem = (sa ? sizeof(ShortlistScratch) : sizeof(MergeScratch)) * G +
-                      sizeof(int) * 2 * static_cast<size_t>(b.N);
+                      sizeof(int) * 2 * static_cast<size_t>(b.N) +
+                      (sizeof(float) + sizeof(int)) * kMaxBeam * kMaxBeam;
   if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
   TailArgs ta{logits, ldl, part_m, part_s, part_arg, part_ld, nsub};
   const ShortlistArgs none{};
