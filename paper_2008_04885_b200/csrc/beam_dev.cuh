@@ -18,10 +18,11 @@ constexpr int kEosIdDev = 3;  // model.hpp:19
 constexpr int kCandPerLane = kMaxBeam * kMaxBeam / 32;  // <= 8
 
 // decode.cpp:64-69 total order: score desc, parent asc, token asc.
+// Branch-free (bitwise on the comparisons): the short-circuit form compiles to
+// divergent branches, ~125 cycles per comparison in a warp-wide rank loop
+// (tools/micro/warp_sort_bench.cu). NaN scores compare false either way.
 __device__ __forceinline__ bool better3(float a, int pa, int ta, float b, int pb, int tb) {
-  if (a != b) return a > b;
-  if (pa != pb) return pa < pb;
-  return ta < tb;
+  return (a > b) | ((a == b) & ((pa < pb) | ((pa == pb) & (ta < tb))));
 }
 
 // Per-sentence beam state, loaded together (one round trip). It is written
@@ -223,7 +224,8 @@ __device__ __forceinline__ void select_sentence_seq(const BeamDev& b, int s, int
 }
 
 // One warp: candidates of sentence s (cand_score / cand_tok of its live rows,
-// or cs_sm / ct_sm in shared memory at [row of the sentence * B + slot])
+// or cs_sm / ct_sm in shared memory at [row of the sentence * B + slot];
+// scratch: 96 words of the warp's shared memory)
 // -> sel_* (surviving hypotheses), finished-list update, termination and the
 // sentence result; writes sent_live[s]. decode.cpp:55-109 with the stable
 // sort of the candidates replaced by ranks in the same total order
@@ -234,7 +236,7 @@ __device__ __forceinline__ void select_sentence_seq(const BeamDev& b, int s, int
 // of this step's, and later ones only replace it on a strictly larger one).
 __device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, int lane,
                                                 const SentState& st,
-                                                const float* cs_sm = nullptr,
+                                                float* scratch, const float* cs_sm = nullptr,
                                                 const int* ct_sm = nullptr) {
   const int kB = min(b.B, b.V);
   if (st.done) return;
@@ -271,17 +273,28 @@ __device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, 
   }
   // decode.cpp:71: take min(|cands|, beam)
   const int n_sel = min(b.B, n_valid);
+  // Ranks: every lane compares its candidate with all others through a
+  // per-warp shared copy (independent broadcast loads; a shuffle-based sort
+  // costs ~200 cycles per dependent stage, tools/micro/warp_sort_bench.cu).
+  float* x_s = scratch;
+  int* x_p = reinterpret_cast<int*>(scratch + 32);
+  int* x_t = reinterpret_cast<int*>(scratch + 64);
+  x_s[lane] = cs;
+  x_p[lane] = cp;
+  x_t[lane] = valid ? ct : INT_MAX;
+  __syncwarp();
   int rank = 0, eos_above = 0;
+#pragma unroll 5
   for (int j = 0; j < nc; ++j) {
-    const float sj = __shfl_sync(0xffffffffu, cs, j);
-    const int pj = __shfl_sync(0xffffffffu, cp, j);
-    const int tj = __shfl_sync(0xffffffffu, ct, j);
-    if (((vmask >> j) & 1u) && better3(sj, pj, tj, cs, cp, ct)) {
-      ++rank;
-      eos_above += tj == kEosIdDev;
-    }
+    const float sj = x_s[j];
+    const int pj = x_p[j], tj = x_t[j];
+    const bool above = tj != INT_MAX && better3(sj, pj, tj, cs, cp, ct);
+    rank += above;
+    eos_above += above && tj == kEosIdDev;
   }
-  const bool sel = valid && rank < n_sel;
+  __syncwarp();
+  const bool valid_sorted = valid;
+  const bool sel = valid_sorted && rank < n_sel;
   const bool eos = sel && ct == kEosIdDev;
   // decode.cpp:77-80 + first max of normalized_score over finished
   const unsigned first_eos = __ballot_sync(0xffffffffu, eos && eos_above == 0);

@@ -39,8 +39,9 @@ constexpr int kMT = 128;                                 // threads per row (4 w
 constexpr int kSubPerThread = kMaxSoftmaxSlices / kMT;  // slices per thread (registers)
 constexpr int kCache = 4;                                // rescanned slices per warp in registers
 
+// Branch-free, as better3 (beam_dev.cuh).
 __device__ __forceinline__ bool better2(float a, int ta, float b, int tb) {
-  return a > b || (a == b && ta < tb);
+  return (a > b) | ((a == b) & (ta < tb));
 }
 
 // Warp-wide argmax of (score desc, token asc); every lane gets the winner.
@@ -527,6 +528,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   int* row0_s = live_s + b.N;
   float* cs_sm = reinterpret_cast<float*>(row0_s + b.N);  // [B rows][B slots]
   int* ct_sm = reinterpret_cast<int*>(cs_sm + kMaxBeam * kMaxBeam);
+  float* sel_scratch = reinterpret_cast<float*>(ct_sm + kMaxBeam * kMaxBeam);  // [96]
   __shared__ int is_last;
   __shared__ SentState st_s;
   const int s = blockIdx.x;
@@ -554,9 +556,9 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 1);
   if (threadIdx.x < 32) {
     if constexpr (MODE == 0)
-      select_sentence(b, s, t, threadIdx.x, st, cs_sm, ct_sm);
+      select_sentence(b, s, t, threadIdx.x, st, sel_scratch, cs_sm, ct_sm);
     else
-      select_sentence(b, s, t, threadIdx.x, st);
+      select_sentence(b, s, t, threadIdx.x, st, sel_scratch);
   }
   if (threadIdx.x == 0) trace_phase_at(b.tr_a, t, 2);
   finish_select(b, t, live_s, row0_s, &is_last, &b.tr_a);
@@ -582,7 +584,7 @@ void launch_topk_select(const float* logits, long long ldl, const float* part_m,
   const int G = std::min(b.B, 8);
   const size_t smem = (sa ? sizeof(ShortlistScratch) : sizeof(MergeScratch)) * G +
                       sizeof(int) * 2 * static_cast<size_t>(b.N) +
-                      (sizeof(float) + sizeof(int)) * kMaxBeam * kMaxBeam;
+                      (sizeof(float) + sizeof(int)) * kMaxBeam * kMaxBeam + sizeof(float) * 96;
   if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
   TailArgs ta{logits, ldl, part_m, part_s, part_arg, part_ld, nsub};
   const ShortlistArgs none{};
