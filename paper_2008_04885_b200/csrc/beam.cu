@@ -48,7 +48,7 @@ constexpr int kSelWarps = 4;
 // Warp per sentence across the grid; the last CTA to finish (atomic ticket)
 // computes the row offsets and writes the compacted rows.
 __global__ void __launch_bounds__(kSelWarps * 32) beam_select_kernel(BeamDev b) {
-  extern __shared__ int sel_smem[];  // [N] new live counts, [N] first rows, [warps][96] scratch
+  extern __shared__ int sel_smem[];  // [N] live counts, [N + N/32 + 1] first rows, [warps][96] scratch
   int* live_s = sel_smem;
   int* row0_s = sel_smem + b.N;
   __shared__ int is_last;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) beam_select_kernel(BeamDev b) 
   trace_begin_at(b.tr_b, t);
   for (int s = s0; s < b.N; s += gridDim.x * nwarps)
     select_sentence(b, s, t, lane, s == s0 ? st0 : load_sent_state(b, s),
-                    reinterpret_cast<float*>(row0_s + b.N) + warp * 96);
+                    reinterpret_cast<float*>(row0_s + b.N + b.N / 32 + 1) + warp * 96);
   finish_select(b, t, live_s, row0_s, &is_last);
   trace_end_at(b.tr_b, t);
 }
@@ -114,7 +114,8 @@ void launch_beam_init(const BeamDev& b, cudaStream_t st) {
 }
 
 void launch_beam_select(const BeamDev& b, cudaStream_t st) {
-  const size_t smem = sizeof(int) * 2 * static_cast<size_t>(b.N) + sizeof(float) * 96 * kSelWarps;
+  const size_t smem = sizeof(int) * (2 * static_cast<size_t>(b.N) + b.N / 32 + 1) +
+                      sizeof(float) * 96 * kSelWarps;
   if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
   ensure_smem_attr(beam_select_kernel, smem);
   launch_k(beam_select_kernel, (b.N + kSelWarps - 1) / kSelWarps, kSelWarps * 32, smem, st, b);

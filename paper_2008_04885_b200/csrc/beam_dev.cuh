@@ -391,6 +391,7 @@ __device__ __forceinline__ void select_sentence(const BeamDev& b, int s, int t, 
 }
 
 // All threads of the CTA: ticket on sel_count; the last CTA of the grid
+// (shared live_s [N], row0_s [N + N / 32 + 1])
 // scans the live counts, writes the compacted rows and advances the step.
 // live_s / row0_s: [N] shared ints; is_last: one shared int.
 __device__ __forceinline__ void finish_select(const BeamDev& b, int t, int* live_s, int* row0_s,
@@ -410,42 +411,65 @@ __device__ __forceinline__ void finish_select(const BeamDev& b, int t, int* live
     __threadfence();
   }
   if (tr && threadIdx.x == 0) trace_phase_at(*tr, t, 3);
-  for (int s = threadIdx.x; s < b.N; s += blockDim.x) live_s[s] = __ldcg(b.sent_live + s);
-  __syncthreads();
-  if (warp == 0) {  // exclusive scan of the live counts (32 sentences per pass)
-    int base = 0;
-    for (int s0 = 0; s0 < b.N; s0 += 32) {
-      const int s = s0 + lane;
-      const int v = s < b.N ? live_s[s] : 0;
-      int inc = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
-      }
-      if (s < b.N) {
-        row0_s[s] = base + inc - v;
-        b.sent_row0[s] = base + inc - v;
-      }
-      base += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (lane == 0) *b.n_rows = base;
-  }
-  __syncthreads();
-  // Compacted rows: thread per (sentence, slot); the selections of a batch of
-  // slots are loaded together before any store (one L2 round trip per batch).
+  // One round trip: the live counts and the first batch of selections (all
+  // slots; the dead ones are filtered after the scan).
   constexpr int kBatch = 4;
   const int total = b.N * b.B;
-  for (int base = threadIdx.x; base < total; base += kBatch * blockDim.x) {
-    int par[kBatch], tok[kBatch];
-    float lp[kBatch];
+  int par[kBatch], tok[kBatch];
+  float lp[kBatch];
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int idx = base + u * blockDim.x;
-      const bool on = idx < total && idx % b.B < live_s[idx / b.B];
-      par[u] = on ? __ldcg(b.sel_parent + idx) : 0;
-      tok[u] = on ? __ldcg(b.sel_tok + idx) : 0;
-      lp[u] = on ? __ldcg(b.sel_lp + idx) : 0.0f;
+  for (int u = 0; u < kBatch; ++u) {
+    const int idx = threadIdx.x + u * blockDim.x;
+    const bool on = idx < total;
+    par[u] = on ? __ldcg(b.sel_parent + idx) : 0;
+    tok[u] = on ? __ldcg(b.sel_tok + idx) : 0;
+    lp[u] = on ? __ldcg(b.sel_lp + idx) : 0.0f;
+  }
+  for (int s = threadIdx.x; s < b.N; s += blockDim.x) live_s[s] = __ldcg(b.sent_live + s);
+  __syncthreads();
+  // Exclusive scan of the live counts: warps scan 32-sentence chunks in
+  // parallel (inclusive, into row0_s), thread 0 chains the chunk totals.
+  const int nwarps = blockDim.x >> 5, nchunks = (b.N + 31) / 32;
+  for (int c = warp; c < nchunks; c += nwarps) {
+    const int s = c * 32 + lane;
+    const int v = s < b.N ? live_s[s] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (s < b.N) row0_s[s] = inc;
+  }
+  __syncthreads();
+  int* chunk_base = row0_s + b.N;  // [N / 32 + 1]
+  if (threadIdx.x == 0) {
+    int base = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      chunk_base[c] = base;
+      base += row0_s[min(b.N, c * 32 + 32) - 1];
+    }
+    *b.n_rows = base;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < b.N; s += blockDim.x) {  // exclusive offsets
+    const int ex = chunk_base[s >> 5] + row0_s[s] - live_s[s];
+    row0_s[s] = ex;
+    b.sent_row0[s] = ex;
+  }
+  __syncthreads();
+  // Compacted rows: thread per (sentence, slot), the first batch already in
+  // registers.
+  for (int base = threadIdx.x; base < total; base += kBatch * blockDim.x) {
+    if (base != threadIdx.x) {
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int idx = base + u * blockDim.x;
+        const bool on = idx < total;
+        par[u] = on ? __ldcg(b.sel_parent + idx) : 0;
+        tok[u] = on ? __ldcg(b.sel_tok + idx) : 0;
+        lp[u] = on ? __ldcg(b.sel_lp + idx) : 0.0f;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {

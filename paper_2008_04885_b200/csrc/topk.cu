@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(TailArgs ta, Shortlis
   Scratch* scr = reinterpret_cast<Scratch*>(tail_smem);
   int* live_s = reinterpret_cast<int*>(scr + G);
   int* row0_s = live_s + b.N;
-  float* cs_sm = reinterpret_cast<float*>(row0_s + b.N);  // [B rows][B slots]
+  float* cs_sm = reinterpret_cast<float*>(row0_s + b.N + b.N / 32 + 1);  // [B rows][B slots]
   int* ct_sm = reinterpret_cast<int*>(cs_sm + kMaxBeam * kMaxBeam);
   float* sel_scratch = reinterpret_cast<float*>(ct_sm + kMaxBeam * kMaxBeam);  // [96]
   __shared__ int is_last;
@@ -583,7 +583,7 @@ void launch_topk_select(const float* logits, long long ldl, const float* part_m,
     fail(kUsageError, "target vocabularies above 32768 are not supported by top-k yet");
   const int G = std::min(b.B, 8);
   const size_t smem = (sa ? sizeof(ShortlistScratch) : sizeof(MergeScratch)) * G +
-                      sizeof(int) * 2 * static_cast<size_t>(b.N) +
+                      sizeof(int) * (2 * static_cast<size_t>(b.N) + b.N / 32 + 1) +
                       (sizeof(float) + sizeof(int)) * kMaxBeam * kMaxBeam + sizeof(float) * 96;
   if (smem > 227 * 1024) fail(kUsageError, "beam search: too many sentences in one batch");
   TailArgs ta{logits, ldl, part_m, part_s, part_arg, part_ld, nsub};
