@@ -240,12 +240,21 @@ def run_gpu(args):
             if rc == 0:
                 kern[name] = dict(ms=ms.value, bytes=by.value, flops=fl.value)
         g = kern["logits_gemm"]
-        ncu = {}
+        # ncu summaries: the latest round's capture of the projection kernel
+        # (DRAM traffic per launch), the measured tensor peaks from round 1.
+        ncu, ncu_r01 = {}, {}
+        for path in (os.path.join(ROOT, "profiles", "r02", "r02_ncu.json"),
+                     os.path.join(ROOT, "profiles", "r01_ncu.json")):
+            try:
+                ncu = json.load(open(path))
+                break
+            except OSError:
+                pass
         try:
-            ncu = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu.json")))
+            ncu_r01 = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu.json")))
         except OSError:
             pass
-        measured = ncu.get("peaks_measured", {})
+        measured = ncu.get("peaks_measured", ncu_r01.get("peaks_measured", {}))
         if prec == mt.INT8:
             tc_frac_peak = measured.get("int8_tops", 2.0 * tc_peak)
             src = ("int8 dense s8 TOPS measured by tools/peaks.py (torch._int_mm 8192^3), "

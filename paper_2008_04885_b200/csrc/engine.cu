@@ -917,6 +917,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
   for (int l = 0; l < c.num_encoder_layers; ++l) {
     EncLayer& L = enc_[l];
     ln_enc(enc_x_.get(), m, L.n1, enc_a_.get(), act_d_);
+    cur_tr_ = enc_trace(l, 0, "enc gemm qkv");
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
     const bool plain = prec_is_tf32x3(act_d_.prec);  // fp32: contexts are the operand
     launch_enc_attention(enc_qkv_.get(), 3 * d, src_off_.get(), n_sent, std::max(max_src, 1), d_,
@@ -933,8 +934,10 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     } else {
       prep_enc(enc_ctx_.get(), d, d_, m, act_d_, false);
     }
+    cur_tr_ = enc_trace(l, 1, "enc gemm wo (+res)");
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
     ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
+    cur_tr_ = enc_trace(l, 2, "enc gemm w1 (+b1, relu)");
     if (plain) {
       gemm(act_d_, L.w1, m, nullptr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
            nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
@@ -950,6 +953,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     } else {
       prep_enc(ffh_.get(), dff_, dff_, m, act_ff_, false);
     }
+    cur_tr_ = enc_trace(l, 3, "enc gemm w2 (+b2, res)");
     gemm(act_ff_, L.w2, m, nullptr, enc_x_.get(), d, L.b2.get(), enc_x_.get(), 0);
   }
   if (c.num_decoder_layers == 0) {
@@ -1010,8 +1014,34 @@ KTrace Engine::next_trace(const char* name) {
   return k;
 }
 
+KTrace Engine::enc_trace(int layer, int slot, const char* name) {
+  KTrace k;
+  if (!trace_ || slot >= kEncTraceSlots || layer >= enc_trace_layers_) return k;
+  if (static_cast<int>(enc_trace_names_.size()) <= slot) enc_trace_names_.resize(slot + 1);
+  enc_trace_names_[slot] = name;
+  k.buf = enc_trace_buf_.get();
+  k.slot = slot;
+  k.per_step = kEncTraceSlots;
+  k.d_step = enc_layer_ids_.get() + layer;
+  return k;
+}
+
 void Engine::trace_reset() {
   if (!trace_) return;
+  const int L = host_.config.num_encoder_layers;
+  if (L > 0) {
+    if (enc_trace_layers_ < L) {
+      enc_layer_ids_.resize(L);
+      std::vector<int> ids(L);
+      for (int i = 0; i < L; ++i) ids[i] = i;
+      enc_layer_ids_.upload(ids.data(), ids.size(), stream_);
+      enc_trace_buf_.resize(size_t(2) * L * kEncTraceSlots);
+      enc_trace_layers_ = L;
+    }
+    std::vector<unsigned long long> e(enc_trace_buf_.size());
+    for (size_t i = 0; i < e.size(); ++i) e[i] = (i & 1) ? 0ull : ~0ull;
+    enc_trace_buf_.upload(e.data(), e.size(), stream_);
+  }
   const size_t need = size_t(2) * T_ * kTraceSlots;
   if (trace_buf_.size() < need) trace_buf_.resize(need);
   std::vector<unsigned long long> init(trace_buf_.size());
@@ -1101,6 +1131,53 @@ std::string Engine::trace_report() {
   std::snprintf(tl, sizeof tl, "  step %.2f us (first kernel's gap: from the previous step's last)\n",
                 total / steps / 1000.0);
   out += tl;
+  // Encoder GEMMs: gap from the previous traced GEMM (the untraced LayerNorm /
+  // attention / quantize kernels in between fall into it), duration; over
+  // layers 1.. (the first follows the embedding).
+  if (enc_trace_layers_ > 0 && !enc_trace_names_.empty()) {
+    std::vector<unsigned long long> e(enc_trace_buf_.size());
+    enc_trace_buf_.download(e.data(), e.size());
+    const int K = kEncTraceSlots, L = enc_trace_layers_;
+    std::vector<double> g(K, 0.0), du(K, 0.0);
+    std::vector<int> ng(K, 0), nd(K, 0);
+    double lay = 0.0;
+    int nl = 0;
+    long long prev_end = -1;
+    long long layer_first = -1, prev_layer_first = -1;
+    for (int l = 0; l < L; ++l) {
+      for (int k = 0; k < K; ++k) {
+        const unsigned long long b0 = e[2 * (size_t(l) * K + k)], b1 = e[2 * (size_t(l) * K + k) + 1];
+        if (b0 == ~0ull || b1 == 0ull) continue;
+        du[k] += double(b1) - double(b0);
+        ++nd[k];
+        if (prev_end >= 0 && l > 0) {
+          g[k] += double(b0) - double(prev_end);
+          ++ng[k];
+        }
+        if (k == 0) {
+          prev_layer_first = layer_first;
+          layer_first = static_cast<long long>(b0);
+          if (prev_layer_first >= 0) {
+            lay += double(layer_first) - double(prev_layer_first);
+            ++nl;
+          }
+        }
+        prev_end = static_cast<long long>(b1);
+      }
+    }
+    out += "encoder (" + std::to_string(L) + " layers, us): gap before / duration\n";
+    for (int k = 0; k < K && k < static_cast<int>(enc_trace_names_.size()); ++k) {
+      if (nd[k] == 0) continue;
+      char line[200];
+      std::snprintf(line, sizeof line, "  %2d %-34s %6.2f  %6.2f\n", k, enc_trace_names_[k].c_str(),
+                    ng[k] ? g[k] / ng[k] / 1000.0 : 0.0, du[k] / nd[k] / 1000.0);
+      out += line;
+    }
+    if (nl > 0) {
+      std::snprintf(tl, sizeof tl, "  layer %.2f us\n", lay / nl / 1000.0);
+      out += tl;
+    }
+  }
   return out;
 }
 

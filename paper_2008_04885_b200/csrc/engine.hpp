@@ -136,6 +136,13 @@ class Engine {
   static constexpr int kTraceSlots = 48;  // timeline slots per decode step
   DeviceBuffer<unsigned long long> trace_buf_;
   DeviceBuffer<unsigned long long> phase_buf_;  // MTG_TRACE=2
+  // Encoder GEMM timeline (MTG_TRACE): slot k of layer l, layer = "step"
+  static constexpr int kEncTraceSlots = 8;
+  DeviceBuffer<unsigned long long> enc_trace_buf_;
+  DeviceBuffer<int> enc_layer_ids_;
+  std::vector<std::string> enc_trace_names_;
+  int enc_trace_layers_ = 0;
+  KTrace enc_trace(int layer, int slot, const char* name);
   bool trace_phases_ = false;
   int trace_slot_ = 0, trace_per_step_ = 0;
   std::vector<std::string> trace_names_;
