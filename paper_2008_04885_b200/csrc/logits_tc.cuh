@@ -44,8 +44,9 @@ __global__ void __launch_bounds__(64 + EG * 256, 1)
   static_assert(2 * kTmemCols <= 512, "two accumulators must fit in TMEM");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, as an offset from the shared array (an integer round
+  // trip of the pointer would turn every shared access generic: LD.E / ST.E).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* staging = reinterpret_cast<float*>(smem + nst * kStageBytes);
   uint64_t* full_bar =
       reinterpret_cast<uint64_t*>(smem + nst * kStageBytes + EG * kEpiStageBytes);

@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(320, 1)
   constexpr int kSubs = kHalf / 32;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, as an offset from the shared array (an integer round
+  // trip of the pointer would turn every shared access generic: LD.E / ST.E).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* staging = reinterpret_cast<float*>(smem + nst * kStageBytes);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * kStageBytes + kEpiStageBytes);
   uint64_t* empty_bar = full_bar + kMaxStages;
