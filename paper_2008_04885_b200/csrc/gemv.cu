@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   pdl_wait();
   pdl_trigger();
   trace_begin(a.trace);
+  if (threadIdx.x == 0) trace_phase(a.trace, 0);
   // Dependent loads, all issued together: live-row count, step, the operand
   // row of this warp (every allocated row; rows >= R are computed and
   // discarded), the first chunk's residual.
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     }
   }
   const int R = min(R_dev, kGemvRows);
+  if (threadIdx.x == 0) trace_phase(a.trace, 1);  // operand row loaded (warp 0)
 
   // ---- step start: beam history reorder (beam.cu beam_reorder_kernel) ----
   if (a.a_mode == 2 && a.reorder && t >= 1 && blockIdx.x == G - 1) {
@@ -358,6 +360,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_phase(a.trace, 2);  // operand rows built
 
   const int gi = warp / ks, kr = warp % ks;  // column group, K range within the CTA's K range
   const int s_begin = kr * kz_steps / ks, s_end = (kr + 1) * kz_steps / ks;
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   for (int i = 0; i < my_count; ++i) {
     const int s = i % nst;
     mbar_wait(&full[s], (i / nst) & 1);
+    if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 3);  // weights landed
     const int cidx = blockIdx.x + i * G;
     const int n0 = cidx * chunk;
     const int ncols = min(chunk, a.N - n0);
@@ -384,6 +388,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       pp[(2 * q + 1) * chunk + c0 + 8] = d[3];
     }
     __syncthreads();  // stage s consumed, partials complete
+    if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 4);  // first chunk's MMAs done
     if (warp == 0 && i + nst < my_count) issue(i + nst);
 
     // Split-K: publish this CTA's sums; the chunk's last CTA adds all splits
@@ -530,6 +535,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     }
     __syncthreads();  // partials reused by the next chunk
   }
+  if (threadIdx.x == 0) trace_phase(a.trace, 5);
   trace_end(a.trace);
 }
 
