@@ -560,33 +560,37 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   const int s = blockIdx.x, h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int r0 = off[s], n = off[s + 1] - r0;
+  // Queries, keys and values of the (sentence, head) staged together (one
+  // round trip; a per-query load of q cost a dependent L2 trip per query).
   float* Ks = sm;
   float* Vs = Ks + max_len * P;
-  float* qs = Vs + max_len * P + warp * (P + ((max_len + 3) & ~3));
-  float* ss = qs + P;
+  float* Qs = Vs + max_len * P;
+  float* ss = Qs + max_len * P + warp * ((max_len + 3) & ~3);
   const float* base = qkv + static_cast<long long>(r0) * ldq + h * dh;
   if constexpr (DH > 0 && DH % 4 == 0) {
     constexpr int Q4 = DH / 4;
     for (int idx = threadIdx.x; idx < n * Q4; idx += blockDim.x) {
       const int j = idx / Q4, c = 4 * (idx - j * Q4);
-      *reinterpret_cast<float4*>(Ks + j * P + c) =
-          *reinterpret_cast<const float4*>(base + j * ldq + d + c);
-      *reinterpret_cast<float4*>(Vs + j * P + c) =
-          *reinterpret_cast<const float4*>(base + j * ldq + 2 * d + c);
+      const float4 kq = *reinterpret_cast<const float4*>(base + j * ldq + d + c);
+      const float4 vq = *reinterpret_cast<const float4*>(base + j * ldq + 2 * d + c);
+      const float4 qq = *reinterpret_cast<const float4*>(base + j * ldq + c);
+      *reinterpret_cast<float4*>(Ks + j * P + c) = kq;
+      *reinterpret_cast<float4*>(Vs + j * P + c) = vq;
+      *reinterpret_cast<float4*>(Qs + j * P + c) = qq;
     }
   } else {
     for (int idx = threadIdx.x; idx < n * dh; idx += blockDim.x) {
       const int j = idx / dh, c = idx - j * dh;
       Ks[j * P + c] = base[j * ldq + d + c];
       Vs[j * P + c] = base[j * ldq + 2 * d + c];
+      Qs[j * P + c] = base[j * ldq + c];
     }
   }
   __syncthreads();
   float mx = 0.0f;
   int bad = 0;
   for (int i = warp; i < n; i += nw) {
-    for (int c = lane; c < dh; c += 32) qs[c] = base[i * ldq + c];
-    __syncwarp();
+    const float* qs = Qs + i * P;
     float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
     attend_warp<DH>(
         qs, n, dh, scale, [&](int j) { return Ks + j * P; }, [&](int j) { return Vs + j * P; },
@@ -1080,7 +1084,7 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
   const int nw = 8;
   const int P = enc_kv_pitch(dh);
   const size_t smem =
-      sizeof(float) * (size_t(max_len) * 2 * P + size_t(nw) * (P + round4(max_len)));
+      sizeof(float) * (size_t(max_len) * 3 * P + size_t(nw) * round4(max_len));
   if (smem > 227 * 1024)
     fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
   auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
