@@ -463,6 +463,44 @@ __global__ void quantize_sent_kernel(const float* __restrict__ x, long long ldx,
   write_operand(op, r, x + r * ldx, n, qscale_of(m), lane, 32);
 }
 
+// Register-resident variant (n % 4 == 0, n <= 128 * V4, 16-byte aligned
+// rows, int8 operand): lane owns elements 4 lane + 128 i, loaded as float4
+// all at once (one round trip; the scalar loop above waits on one load per
+// element group), quantized into 32-bit stores.
+template <int V4>
+__global__ void quantize_sent_vec_kernel(const float* __restrict__ x, long long ldx, int rows,
+                                         int n, const int* __restrict__ row_seg,
+                                         const unsigned* __restrict__ sent_absmax,
+                                         OperandOut op) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + r * ldx;
+  float4 v[V4];
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c = 4 * lane + 128 * i;
+    v[i] = c < n ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float scale = qscale_of(__uint_as_float(sent_absmax[row_seg[r]]));
+  int8_t* qr = op.q + static_cast<long long>(r) * op.k_pad;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c = 4 * lane + 128 * i;
+    if (c < op.k_pad) {
+      const uint32_t w = static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].x, scale))) |
+                         (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].y, scale))) << 8) |
+                         (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].z, scale))) << 16) |
+                         (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v[i].w, scale))) << 24);
+      *reinterpret_cast<uint32_t*>(qr + c) = w;  // columns >= n hold quantized zeros
+    }
+  }
+  for (int c = 128 * V4 + 4 * lane; c < op.k_pad; c += 128) *reinterpret_cast<uint32_t*>(qr + c) = 0u;
+  if (lane == 0) op.row_scale[r] = scale;
+}
+
 // ---- attention ---------------------------------------------------------------------------
 
 // Shared-memory float4 load the compiler cannot hoist out of the key loop
@@ -1061,8 +1099,18 @@ void launch_quantize_sent(const float* x, long long ldx, int rows, int n, const 
                           const unsigned* sent_absmax, const OperandOut& op, cudaStream_t st) {
   if (rows <= 0) return;
   const int wpb = 8;
-  launch_k(quantize_sent_kernel, (rows + wpb - 1) / wpb, wpb * 32, 0, st, x, ldx, rows, n, row_seg,
-           sent_absmax, op);
+  const bool vec = op.prec == 0 && n % 4 == 0 && ldx % 4 == 0 && op.k_pad % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  if (vec && n <= 512) {
+    launch_k(quantize_sent_vec_kernel<4>, (rows + 3) / 4, 4 * 32, 0, st, x, ldx, rows, n, row_seg,
+             sent_absmax, op);
+  } else if (vec && n <= 2048) {
+    launch_k(quantize_sent_vec_kernel<16>, (rows + 3) / 4, 4 * 32, 0, st, x, ldx, rows, n, row_seg,
+             sent_absmax, op);
+  } else {
+    launch_k(quantize_sent_kernel, (rows + wpb - 1) / wpb, wpb * 32, 0, st, x, ldx, rows, n,
+             row_seg, sent_absmax, op);
+  }
   MTG_CUDA(cudaGetLastError());
 }
 
