@@ -520,7 +520,8 @@ __device__ __forceinline__ float4 lds_f4(const float* p) {
 // Key/value rows must be 16-byte aligned when DH % 4 == 0.
 template <int DH, class KP, class VP>
 __device__ __forceinline__ void attend_warp(const float* q, int n, int dh_rt, float scale, KP kp,
-                                            VP vp, float* s, float* out) {
+                                            VP vp, float* s, float* out,
+                                            float* last = nullptr) {
   const int lane = threadIdx.x & 31;
   const int dh = DH > 0 ? DH : dh_rt;
   constexpr bool kVec = DH > 0 && DH % 4 == 0;
@@ -575,6 +576,10 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh_rt, fl
     }
     if (ca < dh) out[ca] = acc_a;
     if (cb < dh) out[cb] = acc_b;
+    if (last) {  // the lane's values of the last column block (all of them for dh <= 64)
+      last[0] = acc_a;
+      last[1] = acc_b;
+    }
   }
   __syncwarp();
 }
@@ -630,9 +635,34 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   for (int i = warp; i < n; i += nw) {
     const float* qs = Qs + i * P;
     float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
+    float vals[2];
     attend_warp<DH>(
         qs, n, dh, scale, [&](int j) { return Ks + j * P; }, [&](int j) { return Vs + j * P; },
-        ss, out);
+        ss, out, vals);
+    // dh <= 64: the lane's two context values are still in registers (a
+    // read-back of the just-written global row costs a round trip per query)
+    if (dh <= 64) {
+      const float va = lane < dh ? vals[0] : 0.0f, vb = 32 + lane < dh ? vals[1] : 0.0f;
+      if (sent_absmax) {
+        mx = fmaxf(mx, fmaxf(fabsf(va), fabsf(vb)));
+        bad |= (lane < dh && !isfinite(va)) | (32 + lane < dh && !isfinite(vb));
+      }
+      if (ctx_lo) {
+        float* lo = ctx_lo + (out - ctx);
+        const float vv[2] = {va, vb};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = lane + 32 * u;
+          if (c < dh) {
+            uint32_t hb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(vv[u]));
+            out[c] = __uint_as_float(hb);
+            lo[c] = __fsub_rn(vv[u], __uint_as_float(hb));
+          }
+        }
+      }
+      continue;
+    }
     if (sent_absmax) {
       for (int c = lane; c < dh; c += 32) {  // lane wrote these itself
         mx = fmaxf(mx, fabsf(out[c]));
