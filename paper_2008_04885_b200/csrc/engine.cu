@@ -924,7 +924,8 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
                          heads_, scale, plain ? act_d_.hi.get() : enc_ctx_.get(),
                          plain ? act_d_.k_pad : d,
                          act_d_.prec == kPrecTF32x3 ? act_d_.lo.get() : nullptr,
-                         fused ? sent_absmax_.get() : nullptr, nonfinite_.get(), stream_);
+                         fused ? sent_absmax_.get() : nullptr, nonfinite_.get(), stream_,
+                         enc_trace(l, 1, "enc attention"));
     count("enc attention");
     if (plain) {
     } else if (fused) {
@@ -934,10 +935,10 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     } else {
       prep_enc(enc_ctx_.get(), d, d_, m, act_d_, false);
     }
-    cur_tr_ = enc_trace(l, 1, "enc gemm wo (+res)");
+    cur_tr_ = enc_trace(l, 2, "enc gemm wo (+res)");
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
     ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
-    cur_tr_ = enc_trace(l, 2, "enc gemm w1 (+b1, relu)");
+    cur_tr_ = enc_trace(l, 3, "enc gemm w1 (+b1, relu)");
     if (plain) {
       gemm(act_d_, L.w1, m, nullptr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
            nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
@@ -953,7 +954,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     } else {
       prep_enc(ffh_.get(), dff_, dff_, m, act_ff_, false);
     }
-    cur_tr_ = enc_trace(l, 3, "enc gemm w2 (+b2, res)");
+    cur_tr_ = enc_trace(l, 4, "enc gemm w2 (+b2, res)");
     gemm(act_ff_, L.w2, m, nullptr, enc_x_.get(), d, L.b2.get(), enc_x_.get(), 0);
   }
   if (c.num_decoder_layers == 0) {
@@ -1023,6 +1024,10 @@ KTrace Engine::enc_trace(int layer, int slot, const char* name) {
   k.slot = slot;
   k.per_step = kEncTraceSlots;
   k.d_step = enc_layer_ids_.get() + layer;
+  if (trace_phases_) {
+    k.ph = enc_phase_buf_.get();
+    k.d_step = enc_layer_ids_.get() + layer;
+  }
   return k;
 }
 
@@ -1036,8 +1041,11 @@ void Engine::trace_reset() {
       for (int i = 0; i < L; ++i) ids[i] = i;
       enc_layer_ids_.upload(ids.data(), ids.size(), stream_);
       enc_trace_buf_.resize(size_t(2) * L * kEncTraceSlots);
+      enc_phase_buf_.resize(size_t(kTracePhases) * L * kEncTraceSlots);
       enc_trace_layers_ = L;
     }
+    std::vector<unsigned long long> z(enc_phase_buf_.size(), 0ull);
+    enc_phase_buf_.upload(z.data(), z.size(), stream_);
     std::vector<unsigned long long> e(enc_trace_buf_.size());
     for (size_t i = 0; i < e.size(); ++i) e[i] = (i & 1) ? 0ull : ~0ull;
     enc_trace_buf_.upload(e.data(), e.size(), stream_);
@@ -1165,6 +1173,11 @@ std::string Engine::trace_report() {
         prev_end = static_cast<long long>(b1);
       }
     }
+    std::vector<unsigned long long> pe;
+    if (trace_phases_) {
+      pe.resize(enc_phase_buf_.size());
+      enc_phase_buf_.download(pe.data(), pe.size());
+    }
     out += "encoder (" + std::to_string(L) + " layers, us): gap before / duration\n";
     for (int k = 0; k < K && k < static_cast<int>(enc_trace_names_.size()); ++k) {
       if (nd[k] == 0) continue;
@@ -1172,6 +1185,26 @@ std::string Engine::trace_report() {
       std::snprintf(line, sizeof line, "  %2d %-34s %6.2f  %6.2f\n", k, enc_trace_names_[k].c_str(),
                     ng[k] ? g[k] / ng[k] / 1000.0 : 0.0, du[k] / nd[k] / 1000.0);
       out += line;
+      if (!pe.empty()) {
+        std::string pl;
+        for (int i = 0; i < kTracePhases; ++i) {
+          double acc = 0.0;
+          int cnt = 0;
+          for (int l = 0; l < L; ++l) {
+            const unsigned long long v = pe[(size_t(l) * K + k) * kTracePhases + i];
+            const unsigned long long b0 = e[2 * (size_t(l) * K + k)];
+            if (v != 0ull && b0 != ~0ull) {
+              acc += double(v) - double(b0);
+              ++cnt;
+            }
+          }
+          if (cnt == 0) continue;
+          char b2[48];
+          std::snprintf(b2, sizeof b2, " p%d %.2f", i, acc / cnt / 1000.0);
+          pl += b2;
+        }
+        if (!pl.empty()) out += "      phases (us after first start):" + pl + "\n";
+      }
     }
     if (nl > 0) {
       std::snprintf(tl, sizeof tl, "  layer %.2f us\n", lay / nl / 1000.0);

@@ -139,6 +139,7 @@ class Engine {
   // Encoder GEMM timeline (MTG_TRACE): slot k of layer l, layer = "step"
   static constexpr int kEncTraceSlots = 8;
   DeviceBuffer<unsigned long long> enc_trace_buf_;
+  DeviceBuffer<unsigned long long> enc_phase_buf_;
   DeviceBuffer<int> enc_layer_ids_;
   std::vector<std::string> enc_trace_names_;
   int enc_trace_layers_ = 0;

@@ -594,9 +594,12 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
                                      const int* __restrict__ off, int d, int dh_rt, int max_len,
                                      float scale, float* __restrict__ ctx, long long ldc,
                                      float* __restrict__ ctx_lo,
-                                     unsigned* __restrict__ sent_absmax, int* nonfinite) {
+                                     unsigned* __restrict__ sent_absmax, int* nonfinite,
+                                     KTrace tr) {
   pdl_wait();
   pdl_trigger();
+  trace_begin(tr);
+  if (threadIdx.x == 0) trace_phase(tr, 0);
   extern __shared__ __align__(16) float sm[];
   const int dh = DH > 0 ? DH : dh_rt;
   const int P = enc_kv_pitch(dh);
@@ -630,6 +633,7 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_phase(tr, 1);
   float mx = 0.0f;
   int bad = 0;
   for (int i = warp; i < n; i += nw) {
@@ -680,11 +684,13 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
       }
     }
   }
+  if (lane == 0) trace_phase(tr, 2);
   if (sent_absmax) {  // the quantize call tensor is the sentence's context block
     mx = warp_allmax(mx);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
     if (lane == 0) atomicMax(sent_absmax + s, __float_as_uint(mx));
   }
+  trace_end(tr);
 }
 
 // CTA epilogue shared by the decoder attention kernels: the context row sits
@@ -1156,7 +1162,8 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
                           int max_len, int d, int heads, float scale, float* ctx, long long ldc,
-                          float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st) {
+                          float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st,
+                          const KTrace& tr) {
   if (n_sent <= 0) return;
   const int dh = d / heads;
   const int nw = 8;
@@ -1168,7 +1175,7 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
   auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
   ensure_smem_attr(k, smem);
   launch_k(k, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale, ctx,
-           ldc, ctx_lo, sent_absmax, nonfinite);
+           ldc, ctx_lo, sent_absmax, nonfinite, tr);
   MTG_CUDA(cudaGetLastError());
 }
 

@@ -118,7 +118,8 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 // tf32 hi, ctx_lo = residual) for the next GEMM.
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
                           int max_len, int d, int heads, float scale, float* ctx, long long ldc,
-                          float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st);
+                          float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st,
+                          const KTrace& tr = {});
 // Encoder LayerNorm -> int8 operand with one scale per sentence (CTA per
 // sentence); zeroes sent_absmax[s] for later accumulation.
 void launch_ln_quant_sent(const float* x, long long ldx, const int* off, int n_sent, int n,
