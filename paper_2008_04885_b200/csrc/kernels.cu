@@ -585,6 +585,7 @@ __device__ __forceinline__ void attend_warp(const float* q, int n, int dh_rt, fl
 }
 
 __host__ __device__ constexpr int enc_kv_pitch(int dh) { return dh % 4 == 0 ? dh + 4 : dh + 1; }
+constexpr int kEncNQ = 4;  // queries per warp attended together (sentences <= 32 tokens)
 
 // Encoder self-attention (model.cpp:418-470 / attention): CTA per (sentence,
 // head). K and V are staged once in smem (row pitch dh+4: conflict-free
@@ -611,7 +612,7 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   float* Ks = sm;
   float* Vs = Ks + max_len * P;
   float* Qs = Vs + max_len * P;
-  float* ss = Qs + max_len * P + warp * ((max_len + 3) & ~3);
+  float* ss = Qs + max_len * P + warp * kEncNQ * ((max_len + 3) & ~3);
   const float* base = qkv + static_cast<long long>(r0) * ldq + h * dh;
   if constexpr (DH > 0 && DH % 4 == 0) {
     constexpr int Q4 = DH / 4;
@@ -636,7 +637,92 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   if (threadIdx.x == 0) trace_phase(tr, 1);
   float mx = 0.0f;
   int bad = 0;
-  for (int i = warp; i < n; i += nw) {
+  // Handles the epilogue of one context value pair of query row i (fp32
+  // context, sentence max / non-finite for int8, TF32 hi + lo for fp32).
+  auto finish = [&](int i, float va, float vb) {
+    float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
+    if (sent_absmax) {
+      mx = fmaxf(mx, fmaxf(fabsf(va), fabsf(vb)));
+      bad |= !isfinite(va) | !isfinite(vb);
+    }
+    if (ctx_lo) {
+      float* lo = ctx_lo + (out - ctx);
+      const float vv[2] = {va, vb};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        uint32_t hb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(vv[u]));
+        out[lane + 32 * u] = __uint_as_float(hb);
+        lo[lane + 32 * u] = __fsub_rn(vv[u], __uint_as_float(hb));
+      }
+    } else {
+      out[lane] = va;
+      out[lane + 32] = vb;
+    }
+  };
+  bool multi = false;
+  if constexpr (DH == 64) {
+    if (n <= 32 && n <= nw * kEncNQ) {
+      multi = true;
+      // Short sentences (n <= 32 keys): each warp attends its up to kEncNQ
+      // queries together -- lane = key for the scores, lane = column pair for
+      // the contexts -- so every key / value load serves all of them and the
+      // queries' dependent chains interleave. Per (query, key) the arithmetic
+      // is attend_warp's: P3 dot over the head dimension, P1 softmax (one key
+      // per lane, then the butterfly), context summed over keys in order.
+      const int nq = (n - warp + nw - 1) / nw;  // this warp's queries: warp + k nw
+      const float* kr = Ks + lane * P;          // rows past n: ignored
+      float acc[kEncNQ];
+#pragma unroll
+      for (int k = 0; k < kEncNQ; ++k) acc[k] = 0.0f;
+#pragma unroll
+      for (int c4 = 0; c4 < DH / 4; ++c4) {
+        const float4 kv = lds_f4(kr + 4 * c4);
+#pragma unroll
+        for (int k = 0; k < kEncNQ; ++k) {
+          if (k < nq) {
+            const float4 qv = lds_f4(Qs + (warp + k * nw) * P + 4 * c4);
+            acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.x, kv.x));
+            acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.y, kv.y));
+            acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.z, kv.z));
+            acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.w, kv.w));
+          }
+        }
+      }
+      const int W4 = (max_len + 3) & ~3;
+#pragma unroll
+      for (int k = 0; k < kEncNQ; ++k) {
+        if (k < nq) {
+          const float v = __fmul_rn(acc[k], scale);
+          const float m = warp_allmax(lane < n ? v : kNegInf);
+          const float e = lane < n ? det_expf_nonpos(__fsub_rn(v, m)) : 0.0f;
+          const float sum = warp_allsum(lane < n ? __fadd_rn(0.0f, e) : 0.0f);
+          if (lane < n) ss[k * W4 + lane] = __fdiv_rn(e, sum);
+        }
+      }
+      __syncwarp();
+      float ca[kEncNQ], cb[kEncNQ];
+#pragma unroll
+      for (int k = 0; k < kEncNQ; ++k) ca[k] = cb[k] = 0.0f;
+      for (int j = 0; j < n; ++j) {
+        const float* vr = Vs + j * P;
+        const float va = vr[lane], vb = vr[32 + lane];
+#pragma unroll
+        for (int k = 0; k < kEncNQ; ++k) {
+          if (k < nq) {
+            const float pj = ss[k * W4 + j];
+            ca[k] = __fadd_rn(ca[k], __fmul_rn(pj, va));
+            cb[k] = __fadd_rn(cb[k], __fmul_rn(pj, vb));
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kEncNQ; ++k)
+        if (k < nq) finish(warp + k * nw, ca[k], cb[k]);
+      __syncwarp();
+    }
+  }
+  for (int i = multi ? n : warp; i < n; i += nw) {
     const float* qs = Qs + i * P;
     float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
     float vals[2];
@@ -1169,7 +1255,7 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
   const int nw = 8;
   const int P = enc_kv_pitch(dh);
   const size_t smem =
-      sizeof(float) * (size_t(max_len) * 3 * P + size_t(nw) * round4(max_len));
+      sizeof(float) * (size_t(max_len) * 3 * P + size_t(nw) * kEncNQ * round4(max_len));
   if (smem > 227 * 1024)
     fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
   auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
