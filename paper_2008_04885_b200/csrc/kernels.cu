@@ -660,9 +660,13 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
       out[lane + 32] = vb;
     }
   };
+  // Queries of this CTA: blockIdx.z of gridDim.z query groups (more CTAs
+  // for batches of few sentences); warp-global index gw of TW warps.
+  const int TW = nw * static_cast<int>(gridDim.z);
+  const int gw = static_cast<int>(blockIdx.z) * nw + warp;
   bool multi = false;
   if constexpr (DH == 64) {
-    if (n <= 32 && n <= nw * kEncNQ) {
+    if (n <= 32 && n <= TW * kEncNQ) {
       multi = true;
       // Short sentences (n <= 32 keys): each warp attends its up to kEncNQ
       // queries together -- lane = key for the scores, lane = column pair for
@@ -670,7 +674,8 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
       // queries' dependent chains interleave. Per (query, key) the arithmetic
       // is attend_warp's: P3 dot over the head dimension, P1 softmax (one key
       // per lane, then the butterfly), context summed over keys in order.
-      const int nq = (n - warp + nw - 1) / nw;  // this warp's queries: warp + k nw
+      // this warp's queries: gw + k TW (query groups over gridDim.z CTAs)
+      const int nq = gw < n ? (n - gw + TW - 1) / TW : 0;
       const float* kr = Ks + lane * P;          // rows past n: ignored
       float acc[kEncNQ];
 #pragma unroll
@@ -681,7 +686,7 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
 #pragma unroll
         for (int k = 0; k < kEncNQ; ++k) {
           if (k < nq) {
-            const float4 qv = lds_f4(Qs + (warp + k * nw) * P + 4 * c4);
+            const float4 qv = lds_f4(Qs + (gw + k * TW) * P + 4 * c4);
             acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.x, kv.x));
             acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.y, kv.y));
             acc[k] = __fadd_rn(acc[k], __fmul_rn(qv.z, kv.z));
@@ -718,11 +723,11 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
       }
 #pragma unroll
       for (int k = 0; k < kEncNQ; ++k)
-        if (k < nq) finish(warp + k * nw, ca[k], cb[k]);
+        if (k < nq) finish(gw + k * TW, ca[k], cb[k]);
       __syncwarp();
     }
   }
-  for (int i = multi ? n : warp; i < n; i += nw) {
+  for (int i = multi ? n : gw; i < n; i += TW) {
     const float* qs = Qs + i * P;
     float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
     float vals[2];
@@ -1260,8 +1265,12 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
     fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
   auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
   ensure_smem_attr(k, smem);
-  launch_k(k, dim3(n_sent, heads), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale, ctx,
-           ldc, ctx_lo, sent_absmax, nonfinite, tr);
+  // Few (sentence, head) CTAs (small batches): split each sentence's
+  // queries over up to 4 CTAs, so more SMs attend (each stages the keys).
+  int qg = 1;
+  while (qg < 4 && n_sent * heads * qg * 2 <= 148 && max_len > nw * qg) qg *= 2;
+  launch_k(k, dim3(n_sent, heads, qg), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale,
+           ctx, ldc, ctx_lo, sent_absmax, nonfinite, tr);
   MTG_CUDA(cudaGetLastError());
 }
 
