@@ -1337,12 +1337,14 @@ void Engine::decoder_body_small(bool reorder) {
     GemvArgs f2 = gemv_args(L.w2);
     rows_from(f2, ffh_.get(), dff_);
     out_to(f2, dec_y_.get(), d, L.b2.get(), true, 0);
-    // fp32 / bf16 FFN-down with a long K: split K over 4 CTAs per column
-    // chunk (more SMs stream the weights; partials added in split order).
-    // int8 rows need their whole-row max, so they stay unsplit.
+    // MTG_GEMV_W2_SPLIT=k: fp32 / bf16 FFN-down split over k CTAs per column
+    // chunk (partials added in split order; int8 rows need their whole-row
+    // max and stay unsplit). Default unsplit: the split's ticket and partial
+    // round trip measured slower at batch 1 (bf16 step 86.5 -> 81.5 us
+    // unsplit, fp32 107.4 -> 105.2 us).
     static const int w2_split = [] {
       const char* e = std::getenv("MTG_GEMV_W2_SPLIT");
-      return e ? std::atoi(e) : 4;
+      return e ? std::atoi(e) : 1;
     }();
     if (prec_ != kINT8 && w2_split > 1 && L.w2.k_pad * (prec_ == kF32 ? 4 : 2) % (w2_split * 128) == 0 &&
         L.w2.k_pad >= 1024) {

@@ -105,6 +105,25 @@ def test_small_batch_matches_tcgen05_path():
     assert a.strip() and a == b
 
 
+def test_small_batch_split_k_w2_agrees():
+    """MTG_GEMV_W2_SPLIT=4 runs the fp32 / bf16 FFN-down GEMV split over four
+    CTAs per column chunk (deterministic last-CTA sum): same hypotheses as
+    the unsplit default, logprobs within the fp32 bar."""
+    code = (
+        "import paper_2008_04885_b200 as mt, oracle_lib as o\n"
+        "c = dict(num_encoder_layers=2, num_decoder_layers=2, d_model=512, d_ff=2048, num_heads=8,"
+        " src_vocab_size=3000, tgt_vocab_size=4000, dropout=0.0, max_seq_len=128)\n"
+        "srcs = o.synthetic_sources(3, 14, 3000, seed=21)\n"
+        "for p in (mt.F32, mt.BF16):\n"
+        "    gm = mt.Model.create(c, seed=5, precision=p)\n"
+        "    out = [gm.translate([s], mt.BeamConfig(5, 0, 1.0))[0] for s in srcs]\n"
+        "    print([(h.tokens, round(h.logprob, 3)) for h in out])\n"
+    )
+    a = _run(code, MTG_GEMV_W2_SPLIT="1")
+    b = _run(code, MTG_GEMV_W2_SPLIT="4")
+    assert a.strip() and a == b
+
+
 @pytest.mark.parametrize("d,heads", [(256, 16), (1024, 16)])
 def test_sixteen_heads_bit_exact(d, heads):
     """More heads than attention warps (8): each warp attends several heads.
