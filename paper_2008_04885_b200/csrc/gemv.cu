@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     const int s = i % nst;
     mbar_wait(&full[s], (i / nst) & 1);
     if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 3);  // weights landed
+    if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 6);  // last chunk landed
     const int cidx = blockIdx.x + i * G;
     const int n0 = cidx * chunk;
     const int ncols = min(chunk, a.N - n0);
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     }
     __syncthreads();  // stage s consumed, partials complete
     if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 4);  // first chunk's MMAs done
+    if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 7);  // last chunk's MMAs done
     if (warp == 0 && i + nst < my_count) issue(i + nst);
 
     // Split-K: publish this CTA's sums; the chunk's last CTA adds all splits
