@@ -114,6 +114,32 @@ __device__ __forceinline__ void mma_step(uint32_t (&d)[4], const uint8_t* wf, co
   }
 }
 
+// fp32 (TF32x3) with the three products in separate accumulators: three
+// independent MMA chains instead of one chain three times as long (the MMA
+// phase of the batch-1 projection GEMV is latency-bound on that chain).
+// Final value (lo.hi + hi.lo) + hi.hi.
+__device__ __forceinline__ void mma_step_tf32x3(uint32_t (&d_lh)[4], uint32_t (&d_hl)[4],
+                                                uint32_t (&d_hh)[4], const uint8_t* wf,
+                                                const uint8_t* xf) {
+  const uint4 av = *reinterpret_cast<const uint4*>(wf);
+  const uint32_t a[4] = {av.x, av.y, av.z, av.w};
+  const uint32_t b[2] = {*reinterpret_cast<const uint32_t*>(xf), *reinterpret_cast<const uint32_t*>(xf + 16)};
+  uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ah[i] = tf32_hi(a[i]);
+    al[i] = __float_as_uint(__fsub_rn(__uint_as_float(a[i]), __uint_as_float(ah[i])));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    bh[i] = tf32_hi(b[i]);
+    bl[i] = __float_as_uint(__fsub_rn(__uint_as_float(b[i]), __uint_as_float(bh[i])));
+  }
+  mma_frag<2>(d_lh, al, bh);
+  mma_frag<2>(d_hl, ah, bl);
+  mma_frag<2>(d_hh, ah, bh);
+}
+
 // Stores one operand element (row n, column c of the CTA's K range; pitch P).
 template <int PREC>
 __device__ __forceinline__ void store_elem(uint8_t* A, int P, int n, int c, float x, int8_t q) {
@@ -379,8 +405,19 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       const uint8_t* wf = stages + s * L.stage_bytes + gi * kz_steps * 512 + lane * 16;
       const uint8_t* xf = A + g * AP + 4 * q;  // operand row g, the lane's K bytes
       uint32_t d[4] = {0u, 0u, 0u, 0u};
+      if constexpr (PREC == 2) {
+        uint32_t d1[4] = {0u, 0u, 0u, 0u}, d2[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 4
-      for (int st = s_begin; st < s_end; ++st) mma_step<PREC>(d, wf + st * 512, xf + st * kKStepBytes);
+        for (int st = s_begin; st < s_end; ++st)
+          mma_step_tf32x3(d1, d2, d, wf + st * 512, xf + st * kKStepBytes);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          d[e] = __float_as_uint(__fadd_rn(
+              __fadd_rn(__uint_as_float(d1[e]), __uint_as_float(d2[e])), __uint_as_float(d[e])));
+      } else {
+#pragma unroll 4
+        for (int st = s_begin; st < s_end; ++st) mma_step<PREC>(d, wf + st * 512, xf + st * kKStepBytes);
+      }
       uint32_t* pp = part + kr * kGemvRows * chunk;
       const int c0 = gi * 16 + g;
       pp[(2 * q) * chunk + c0] = d[0];
