@@ -102,6 +102,7 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
         case 32: return launch_one<PREC, 32, kEpiTf32Out>(p, ep, stream);
         case 64: return launch_one<PREC, 64, kEpiTf32Out>(p, ep, stream);
         case 128: return launch_one<PREC, 128, kEpiTf32Out>(p, ep, stream);
+        case 192: return launch_one<PREC, 192, kEpiTf32Out>(p, ep, stream);
         case 256: return launch_one<PREC, 256, kEpiTf32Out>(p, ep, stream);
       }
     }
@@ -113,6 +114,7 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
       case 32: return launch_one<PREC, 32, kEpiSegMax>(p, ep, stream);
       case 64: return launch_one<PREC, 64, kEpiSegMax>(p, ep, stream);
       case 128: return launch_one<PREC, 128, kEpiSegMax>(p, ep, stream);
+      case 192: return launch_one<PREC, 192, kEpiSegMax>(p, ep, stream);
       case 256: return launch_one<PREC, 256, kEpiSegMax>(p, ep, stream);
     }
   }
@@ -134,6 +136,7 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
     case 32: return launch_one<PREC, 32, kEpiLinear>(p, ep, stream);
     case 64: return launch_one<PREC, 64, kEpiLinear>(p, ep, stream);
     case 128: return launch_one<PREC, 128, kEpiLinear>(p, ep, stream);
+    case 192: return launch_one<PREC, 192, kEpiLinear>(p, ep, stream);
     case 256: return launch_one<PREC, 256, kEpiLinear>(p, ep, stream);
   }
   fail(kStateError, "gemm: unsupported tile width");
@@ -241,6 +244,18 @@ GemmPlan plan_gemm(const Operand& a, const Operand& b, int m_max, int n, int for
   const bool ffn_up_deep = !force_bn && bn == 32 && prec_is_tf32x3(b.prec) && p.m_tiles >= 3 &&
                            n >= 4 * a.k_pad && a.k_pad >= 256;
   if (ffn_up_deep) bn = 64;
+  // 128-column tiles just over one wave at one CTA per SM (the encoder's
+  // fp32 QKV / FFN-up at batch 64: 156 / 208 tiles on 148 SMs, a second wave
+  // of 8 / 60 tiles): 192-column tiles fit one wave (104 / 143 tiles).
+  // Measured fp32 QKV 29.4 -> 19.7 us, FFN-up 35.9 -> 24.8 us; bf16 QKV
+  // 8.8 -> 8.0 us (its FFN-up neutral); int8 slower (two CTAs per SM).
+  {
+    const int t128 = p.m_tiles * ((n + 127) / 128), t192 = p.m_tiles * ((n + 191) / 192);
+    const bool fits = bn == 128 && t128 > 148 && t192 <= 148;
+    if (!force_bn && fits &&
+        (prec_is_tf32x3(b.prec) || (b.prec == kPrecBF16 && n % 192 == 0)))
+      bn = 192;
+  }
   // Just under one tile per SM at 32 columns (the fused QKV GEMM at batch 64:
   // 144 tiles, split 2): 64-column tiles split 3-4 ways read the activation
   // rows half as often (measured int8 5.2 -> 4.5 us, fp32 11.6 -> 11.2 us).
