@@ -507,7 +507,7 @@ void Engine::prep(const float* x, long long ldx, int k, int max_rows, const int*
 void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
                   long long ldc, const float* bias, const float* residual, int relu,
                   long long c_step_stride, const int* d_step, unsigned* seg_absmax,
-                  float* c_lo) {
+                  float* c_lo, bool bf16_out) {
   auto& cache = plan_cache();
   PlanKey key{a.op().ptr, w.op().ptr, m};
   auto it = cache.find(key);
@@ -534,6 +534,7 @@ void Engine::gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m
   ep.d_M = d_m;
   ep.N = w.n;
   ep.C_lo = c_lo;
+  ep.bf16_out = bf16_out ? 1 : 0;
   ep.tr = cur_tr_;
   cur_tr_ = KTrace{};
   if (seg_absmax) {
@@ -913,6 +914,11 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
   }();
   const bool fused = prec_ == kINT8 && d_ <= 512 && !no_enc_fusion;
   enc_fused_ = fused;
+  // MTG_BF16_DIRECT=0: bf16 contexts / hidden rows through cast kernels (A/B)
+  static const bool bf16_direct_ok = [] {
+    const char* e = std::getenv("MTG_BF16_DIRECT");
+    return !(e && e[0] == '0');
+  }();
   const OperandOut od = opout(act_d_), off_ = opout(act_ff_);
   for (int l = 0; l < c.num_encoder_layers; ++l) {
     EncLayer& L = enc_[l];
@@ -920,14 +926,20 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     cur_tr_ = enc_trace(l, 0, "enc gemm qkv");
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
     const bool plain = prec_is_tf32x3(act_d_.prec);  // fp32: contexts are the operand
+    // bf16 (head dim 64, unpadded rows): the attention writes the bf16
+    // operand and the FFN-up GEMM its bf16 hidden operand (no cast kernels)
+    const bool bf16_direct = bf16_direct_ok && prec_ == kBF16 && d_ / heads_ == 64 &&
+                             act_d_.k_pad == d_ && act_ff_.k_pad == dff_;
+    float* const ctx_out = plain ? act_d_.hi.get()
+                           : bf16_direct ? reinterpret_cast<float*>(act_d_.h.get())
+                                         : enc_ctx_.get();
     launch_enc_attention(enc_qkv_.get(), 3 * d, src_off_.get(), n_sent, std::max(max_src, 1), d_,
-                         heads_, scale, plain ? act_d_.hi.get() : enc_ctx_.get(),
-                         plain ? act_d_.k_pad : d,
+                         heads_, scale, ctx_out, plain || bf16_direct ? act_d_.k_pad : d,
                          act_d_.prec == kPrecTF32x3 ? act_d_.lo.get() : nullptr,
                          fused ? sent_absmax_.get() : nullptr, nonfinite_.get(), stream_,
-                         enc_trace(l, 1, "enc attention"));
+                         enc_trace(l, 1, "enc attention"), bf16_direct);
     count("enc attention");
-    if (plain) {
+    if (plain || bf16_direct) {
     } else if (fused) {
       launch_quantize_sent(enc_ctx_.get(), d, m, d_, src_rowseg_.get(), sent_absmax_.get(), od,
                            stream_);
@@ -942,11 +954,14 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     if (plain) {
       gemm(act_d_, L.w1, m, nullptr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
            nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
+    } else if (bf16_direct) {
+      gemm(act_d_, L.w1, m, nullptr, reinterpret_cast<float*>(act_ff_.h.get()), act_ff_.k_pad,
+           L.b1.get(), nullptr, 1, 0, nullptr, nullptr, nullptr, true);
     } else {
       gemm(act_d_, L.w1, m, nullptr, ffh_.get(), dff_, L.b1.get(), nullptr, 1, 0, nullptr,
            fused ? sent_absmax_.get() : nullptr);
     }
-    if (plain) {
+    if (plain || bf16_direct) {
     } else if (fused) {
       launch_quantize_sent(ffh_.get(), dff_, m, dff_, src_rowseg_.get(), sent_absmax_.get(), off_,
                            stream_);

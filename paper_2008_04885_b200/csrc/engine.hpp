@@ -116,7 +116,7 @@ class Engine {
   void gemm(const ActOperand& a, const DevLinear& w, int m, const int* d_m, float* c,
             long long ldc, const float* bias, const float* residual, int relu,
             long long c_step_stride = 0, const int* d_step = nullptr,
-            unsigned* seg_absmax = nullptr, float* c_lo = nullptr);
+            unsigned* seg_absmax = nullptr, float* c_lo = nullptr, bool bf16_out = false);
   // Output projection into logits_ plus the per-slice softmax partials.
   void gemm_logits(int m, const int* d_m);
   int stage_sources(const std::vector<std::vector<int>>& srcs, std::vector<int>& status);

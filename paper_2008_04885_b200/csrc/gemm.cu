@@ -108,6 +108,18 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
     }
     fail(kStateError, "gemm: TF32 operand output needs a TF32x3 GEMM");
   }
+  if (ep.bf16_out) {
+    if constexpr (PREC == kPrecBF16) {
+      switch (p.bn) {
+        case 32: return launch_one<PREC, 32, kEpiBf16Out>(p, ep, stream);
+        case 64: return launch_one<PREC, 64, kEpiBf16Out>(p, ep, stream);
+        case 128: return launch_one<PREC, 128, kEpiBf16Out>(p, ep, stream);
+        case 192: return launch_one<PREC, 192, kEpiBf16Out>(p, ep, stream);
+        case 256: return launch_one<PREC, 256, kEpiBf16Out>(p, ep, stream);
+      }
+    }
+    fail(kStateError, "gemm: bf16 operand output needs a bf16 GEMM");
+  }
   if (ep.seg_absmax) {
     if (ep.residual) fail(kStateError, "gemm: segment-max epilogue takes no residual");
     switch (p.bn) {

@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include "detmath.cuh"
 #include "launch.cuh"
@@ -63,18 +64,26 @@ struct GemmEpilogue {
   // Optional: write the output as a TF32x3 operand, C = tf32(y), C_lo = y - C
   // (the next GEMM's A), instead of plain y.
   float* C_lo;
+  // Optional: write the output as a bf16 operand (C then points at the bf16
+  // buffer, reinterpreted; element offsets as for fp32).
+  int bf16_out;
   KTrace tr;  // MTG_TRACE timeline slot
   int split_dist;  // split-K sums by all epilogue threads (1) or per owner warp (0)
 };
 
-// Stores y at C[off] (or its tf32 hi / lo split for the kEpiTf32Out epilogue).
-template <bool kTf32Out>
-__device__ __forceinline__ void gemm_store(float* C, float* C_lo, long long off, float y) {
-  if constexpr (kTf32Out) {
+// Stores y at C[off] (or its tf32 hi / lo split for the kEpiTf32Out
+// epilogue, or its bf16 rounding for kEpiBf16Out: C0 is the buffer base, the
+// element index is (C - C0) + off).
+template <int EPIK>
+__device__ __forceinline__ void gemm_store(float* C, float* C_lo, long long off, float y,
+                                           float* C0) {
+  if constexpr (EPIK == 3) {  // kEpiTf32Out
     uint32_t hb;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(y));
     C[off] = __uint_as_float(hb);
     C_lo[off] = __fsub_rn(y, __uint_as_float(hb));
+  } else if constexpr (EPIK == 4) {  // kEpiBf16Out
+    reinterpret_cast<__nv_bfloat16*>(C0)[(C - C0) + off] = __float2bfloat16_rn(y);
   } else {
     C[off] = y;
   }
@@ -86,6 +95,7 @@ constexpr int kEpiLinear = 0;
 constexpr int kEpiSoftmaxParts = 1;
 constexpr int kEpiSegMax = 2;  // linear + per-segment max |y| (bias/ReLU in phase 1)
 constexpr int kEpiTf32Out = 3;  // linear, output written as a TF32x3 operand (hi + lo)
+constexpr int kEpiBf16Out = 4;  // linear, output written as a bf16 operand
 
 // kPrecTF32x3A: TF32x3 whose A operand arrives as plain fp32 and is split
 // into hi + lo inside the kernel (half the activation bytes); B as kPrecTF32x3.
@@ -571,7 +581,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
           if (has_bias && !seg_mode) x = __fadd_rn(x, bias_pre);
           if (relu && !seg_mode) x = x > 0.0f ? x : 0.0f;
           if (has_res) x = __fadd_rn(res_pre[i], x);
-          if (col_ok && i < nrows) gemm_store<EPI == kEpiTf32Out>(cp, cp_lo, i * ldc, x);
+          if (col_ok && i < nrows) gemm_store<EPI>(cp, cp_lo, i * ldc, x, ep.C);
         }
         __syncwarp();
         continue;
@@ -580,7 +590,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
         if (col_ok) {
 #pragma unroll 8
           for (int i = 0; i < 32; ++i)
-            if (i < nrows) gemm_store<EPI == kEpiTf32Out>(cp, cp_lo, i * ldc, stage[i * 33 + lane]);
+            if (i < nrows) gemm_store<EPI>(cp, cp_lo, i * ldc, stage[i * 33 + lane], ep.C);
         }
         __syncwarp();
         continue;
@@ -603,7 +613,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
           if (has_bias) x = __fadd_rn(x, bias);
           if (relu) x = x > 0.0f ? x : 0.0f;
           if (has_res) x = __fadd_rn(res[i], x);
-          if (col_ok && i0 + i < nrows) gemm_store<EPI == kEpiTf32Out>(cp, cp_lo, (i0 + i) * ldc, x);
+          if (col_ok && i0 + i < nrows) gemm_store<EPI>(cp, cp_lo, (i0 + i) * ldc, x, ep.C);
         }
       }
       __syncwarp();

@@ -596,7 +596,7 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
                                      float scale, float* __restrict__ ctx, long long ldc,
                                      float* __restrict__ ctx_lo,
                                      unsigned* __restrict__ sent_absmax, int* nonfinite,
-                                     KTrace tr) {
+                                     KTrace tr, int out_bf16) {
   pdl_wait();
   pdl_trigger();
   trace_begin(tr);
@@ -613,6 +613,7 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   float* Vs = Ks + max_len * P;
   float* Qs = Vs + max_len * P;
   float* ss = Qs + max_len * P + warp * kEncNQ * ((max_len + 3) & ~3);
+  float* gscratch = Qs + max_len * P + nw * kEncNQ * ((max_len + 3) & ~3) + warp * 64;
   const float* base = qkv + static_cast<long long>(r0) * ldq + h * dh;
   if constexpr (DH > 0 && DH % 4 == 0) {
     constexpr int Q4 = DH / 4;
@@ -641,6 +642,13 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   // context, sentence max / non-finite for int8, TF32 hi + lo for fp32).
   auto finish = [&](int i, float va, float vb) {
     float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
+    if (out_bf16) {  // ctx is the bf16 operand of the Wo GEMM (reinterpreted)
+      __nv_bfloat16* o =
+          reinterpret_cast<__nv_bfloat16*>(ctx) + static_cast<long long>(r0 + i) * ldc + h * dh;
+      o[lane] = __float2bfloat16_rn(va);
+      o[lane + 32] = __float2bfloat16_rn(vb);
+      return;
+    }
     if (sent_absmax) {
       mx = fmaxf(mx, fmaxf(fabsf(va), fabsf(vb)));
       bad |= !isfinite(va) | !isfinite(vb);
@@ -729,11 +737,15 @@ __global__ void enc_attention_kernel(const float* __restrict__ qkv, long long ld
   }
   for (int i = multi ? n : gw; i < n; i += TW) {
     const float* qs = Qs + i * P;
-    float* out = ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
+    float* out = out_bf16 ? gscratch : ctx + static_cast<long long>(r0 + i) * ldc + h * dh;
     float vals[2];
     attend_warp<DH>(
         qs, n, dh, scale, [&](int j) { return Ks + j * P; }, [&](int j) { return Vs + j * P; },
         ss, out, vals);
+    if (out_bf16) {  // dh == 64 (host): the values are in registers
+      finish(i, vals[0], vals[1]);
+      continue;
+    }
     // dh <= 64: the lane's two context values are still in registers (a
     // read-back of the just-written global row costs a round trip per query)
     if (dh <= 64) {
@@ -1254,13 +1266,13 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
                           int max_len, int d, int heads, float scale, float* ctx, long long ldc,
                           float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st,
-                          const KTrace& tr) {
+                          const KTrace& tr, bool out_bf16) {
   if (n_sent <= 0) return;
   const int dh = d / heads;
   const int nw = 8;
   const int P = enc_kv_pitch(dh);
   const size_t smem =
-      sizeof(float) * (size_t(max_len) * 3 * P + size_t(nw) * kEncNQ * round4(max_len));
+      sizeof(float) * (size_t(max_len) * 3 * P + size_t(nw) * (kEncNQ * round4(max_len) + 64));
   if (smem > 227 * 1024)
     fail(kUsageError, "encoder attention: sentence x head dimension too large for smem");
   auto k = dh == 64 ? enc_attention_kernel<64> : enc_attention_kernel<0>;
@@ -1269,8 +1281,9 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
   // queries over up to 4 CTAs, so more SMs attend (each stages the keys).
   int qg = 1;
   while (qg < 4 && n_sent * heads * qg * 2 <= 148 && max_len > nw * qg) qg *= 2;
+  if (out_bf16 && dh != 64) fail(kStateError, "encoder attention: bf16 output needs head dim 64");
   launch_k(k, dim3(n_sent, heads, qg), nw * 32, smem, st, qkv, ldq, off, d, dh, max_len, scale,
-           ctx, ldc, ctx_lo, sent_absmax, nonfinite, tr);
+           ctx, ldc, ctx_lo, sent_absmax, nonfinite, tr, out_bf16 ? 1 : 0);
   MTG_CUDA(cudaGetLastError());
 }
 

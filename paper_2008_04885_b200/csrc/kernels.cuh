@@ -119,7 +119,8 @@ void launch_quantize_seg(const float* x, long long ldx, int rows, int n, const i
 void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n_sent,
                           int max_len, int d, int heads, float scale, float* ctx, long long ldc,
                           float* ctx_lo, unsigned* sent_absmax, int* nonfinite, cudaStream_t st,
-                          const KTrace& tr = {});
+                          const KTrace& tr = {},
+                          bool out_bf16 = false);
 // Encoder LayerNorm -> int8 operand with one scale per sentence (CTA per
 // sentence); zeroes sent_absmax[s] for later accumulation.
 void launch_ln_quant_sent(const float* x, long long ldx, const int* off, int n_sent, int n,

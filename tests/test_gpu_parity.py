@@ -341,6 +341,32 @@ def test_step_fusion_modes_agree():
 
 
 @pytest.mark.gpu
+def test_bf16_direct_operands_agree():
+    """bf16 encoder: the attention and the FFN-up GEMM write the bf16
+    operands themselves (default) or through cast kernels
+    (MTG_BF16_DIRECT=0): both round the same fp32 values, so the results are
+    identical."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2008_04885_b200 as mt, oracle_lib as o\n"
+        "from golden_util import f32hex\n"
+        "c = dict(num_encoder_layers=2, num_decoder_layers=2, d_model=128, d_ff=512, num_heads=2,"
+        " src_vocab_size=700, tgt_vocab_size=900, dropout=0.0, max_seq_len=64)\n"
+        "gm = mt.Model.create(c, seed=3, precision=mt.BF16)\n"
+        "srcs = o.synthetic_sources(12, 9, 700, seed=2) + o.synthetic_sources(3, 40, 700, seed=5)\n"
+        "print([(h.tokens, f32hex(h.logprob)) for h in gm.translate(srcs, mt.BeamConfig(5, 0, 1.0))])\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("1", "0"):
+        env = dict(os.environ, MTG_BF16_DIRECT=v)
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, check=True,
+                                   capture_output=True, text=True).stdout)
+    assert outs[0].strip() and outs[0] == outs[1]
+
+
+@pytest.mark.gpu
 def test_f32_projection_kernels_agree():
     """The fp32 output projection runs on CTA pairs (cta_group::2, default),
     one persistent CTA per tile (MTG_LOGITS_PAIR=0) or one tile per CTA
