@@ -1522,9 +1522,16 @@ void Engine::decoder_body(bool reorder) {
     gemm(act_d_, L.cross_wo, R, dr, dec_y_.get(), d, nullptr, dec_y_.get(), 0);
     ln_dec(L.n3);
     cur_tr_ = next_trace("gemm w1 (+b1, relu)");
+    static const bool bf16_direct = [] {  // MTG_BF16_DIRECT=0: cast kernel (A/B)
+      const char* e = std::getenv("MTG_BF16_DIRECT");
+      return !(e && e[0] == '0');
+    }();
     if (prec_is_tf32x3(act_ff_.prec)) {  // FFN-up writes the FFN-down operand itself
       gemm(act_d_, L.w1, R, dr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
            nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
+    } else if (bf16_direct && prec_ == kBF16 && act_ff_.k_pad == dff_) {  // ... as bf16
+      gemm(act_d_, L.w1, R, dr, reinterpret_cast<float*>(act_ff_.h.get()), act_ff_.k_pad,
+           L.b1.get(), nullptr, 1, 0, nullptr, nullptr, nullptr, true);
     } else {
       gemm(act_d_, L.w1, R, dr, ffh_.get(), dff_, L.b1.get(), nullptr, 1);
       prep(ffh_.get(), dff_, dff_, R, dr, nullptr, 0, act_ff_);
