@@ -135,6 +135,9 @@ void launch_prec(const GemmPlan& p, const GemmEpilogue& ep, cudaStream_t stream)
   const int fl = (ep.bias ? 1 : 0) | (ep.relu ? 2 : 0) | (ep.residual ? 4 : 0) |
                  (ep.d_step ? 8 : 0);
   if (p.bn == 64 && fl == 5) return launch_one<PREC, 64, kEpiLinear, 5>(p, ep, stream);  // FFN-down
+  // 64-column QKV at batch 64 (KV-cache slab offset only): the generic
+  // variant spills for int8
+  if (p.bn == 64 && fl == 8) return launch_one<PREC, 64, kEpiLinear, 8>(p, ep, stream);
   if (p.bn == 32) {
     switch (fl) {
       case 0: return launch_one<PREC, 32, kEpiLinear, 0>(p, ep, stream);
