@@ -85,6 +85,32 @@ def test_encode_and_step_logits(config):
             assert rel(lg, ref_lg) < 1e-4
 
 
+@pytest.mark.parametrize("batch", [1, 6], ids=["b1", "b6"])
+def test_encoder_long_and_short_sentences_bit_exact(batch):
+    """Encoder attention paths: sentences up to 32 tokens (a warp's queries
+    attended together; split over several CTAs at small batches) and longer
+    ones (query per warp), mixed in one batch; int8 encoder states and
+    forced logits bit-exact against the oracle, fp32 within 1e-4."""
+    c = cfg(2, 1, 64, 128, 1, 500, 300, 128)  # one head of 64
+    om = o.OracleModel.create(c, seed=11)
+    lens = [5, 31, 33, 60, 17, 45][:batch] if batch > 1 else [47]
+    srcs = [o.synthetic_sources(1, n, c["src_vocab_size"], seed=40 + n)[0] for n in lens]
+    forced = [4, 5, 6]
+    for prec in (mt.INT8, mt.F32):
+        gm = mt.Model.create(c, seed=11, precision=prec)
+        int8 = prec == mt.INT8
+        enc = gm.encode(srcs)
+        ref_enc = np.concatenate([om.encode(s, int8) for s in srcs])
+        lg = gm.forced_logits(srcs, forced)
+        ref_lg = np.stack([om.forced_logits(s, forced, int8) for s in srcs])
+        if int8:
+            assert np.array_equal(enc, ref_enc)
+            assert np.array_equal(lg, ref_lg)
+        else:
+            assert rel(enc, ref_enc) < 1e-4
+            assert rel(lg, ref_lg) < 1e-4
+
+
 def test_incremental_matches_teacher_forced_on_gpu():  # test_model.cpp:211-228, C2
     worst = 0.0
     for trial in range(12):
