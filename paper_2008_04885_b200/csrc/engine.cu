@@ -788,8 +788,11 @@ void Engine::prep_enc(const float* x, long long ldx, int k, int m, ActOperand& o
 // Encoder LayerNorm; int8 also records per-row max |y| for the segment scale.
 void Engine::ln_enc(const float* x, int m, const LN& ln, float* y, ActOperand& out) {
   if (prec_ == kINT8 && enc_fused_) {  // fused LN + per-sentence quantization
+    OperandOut o = opout(out);
+    o.tr = enc_ln_tr_;
+    enc_ln_tr_ = KTrace{};
     launch_ln_quant_sent(x, d_, src_off_.get(), enc_n_sent_, d_, ln.g.get(), ln.b.get(), y, d_,
-                         opout(out), sent_absmax_.get(), stream_);
+                         o, sent_absmax_.get(), stream_, std::max(enc_max_src_, 1));
     count("enc layernorm+quantize");
     return;
   }
@@ -905,6 +908,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
                    stream_);
   count("enc embed");
   enc_n_sent_ = n_sent;
+  enc_max_src_ = max_src;
   // int8 with d <= 512: the LayerNorms quantize per sentence themselves and
   // zero the sentence max that attention / the FFN-up epilogue accumulate,
   // so each remaining quantize is a single pass (9 kernels per layer).
@@ -922,6 +926,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
   const OperandOut od = opout(act_d_), off_ = opout(act_ff_);
   for (int l = 0; l < c.num_encoder_layers; ++l) {
     EncLayer& L = enc_[l];
+    enc_ln_tr_ = enc_trace(l, 5, "enc layernorm 1");
     ln_enc(enc_x_.get(), m, L.n1, enc_a_.get(), act_d_);
     cur_tr_ = enc_trace(l, 0, "enc gemm qkv");
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
@@ -949,6 +954,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     }
     cur_tr_ = enc_trace(l, 2, "enc gemm wo (+res)");
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
+    enc_ln_tr_ = enc_trace(l, 6, "enc layernorm 2");
     ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
     cur_tr_ = enc_trace(l, 3, "enc gemm w1 (+b1, relu)");
     if (plain) {

@@ -144,6 +144,7 @@ class Engine {
   std::vector<std::string> enc_trace_names_;
   int enc_trace_layers_ = 0;
   KTrace enc_trace(int layer, int slot, const char* name);
+  KTrace enc_ln_tr_;  // timeline slot of the next encoder LayerNorm (int8 fused)
   bool trace_phases_ = false;
   int trace_slot_ = 0, trace_per_step_ = 0;
   std::vector<std::string> trace_names_;
@@ -229,6 +230,7 @@ class Engine {
   std::vector<int> sl_status_;  // per staged sentence: shortlist validation status
   ShortlistArgs shortlist_args() const;  // per-sentence max |x| (float bits), encoder int8
   int enc_n_sent_ = 0;
+  int enc_max_src_ = 0;  // longest source of the running encoder batch
   bool enc_fused_ = false;
   bool split_k_ = true;
   long long part_ld_ = 0;

@@ -125,7 +125,8 @@ void launch_enc_attention(const float* qkv, long long ldq, const int* off, int n
 // sentence); zeroes sent_absmax[s] for later accumulation.
 void launch_ln_quant_sent(const float* x, long long ldx, const int* off, int n_sent, int n,
                           const float* g, const float* b, float* y, long long ldy,
-                          const OperandOut& op, unsigned* sent_absmax, cudaStream_t st);
+                          const OperandOut& op, unsigned* sent_absmax, cudaStream_t st,
+                          int max_rows = 0);
 // int8 operand rows scaled by their sentence's accumulated max |x|.
 void launch_quantize_sent(const float* x, long long ldx, int rows, int n, const int* row_seg,
                           const unsigned* sent_absmax, const OperandOut& op, cudaStream_t st);
