@@ -391,13 +391,14 @@ __global__ void __launch_bounds__(1024)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int r0 = off[s], r1 = off[s + 1];
   const bool staged = stage_rows >= r1 - r0;
-  float gv[KPL], bv[KPL];
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const int c = lane + 32 * i;
-    gv[i] = c < n ? g[c] : 0.0f;
-    bv[i] = c < n ? b[c] : 0.0f;
+  // gain / bias in shared memory (in registers they push the 16-value rows
+  // past the 64-register cap of 1024 threads: spills)
+  __shared__ float gs[32 * KPL], bs[32 * KPL];
+  for (int c = threadIdx.x; c < 32 * KPL; c += blockDim.x) {
+    gs[c] = c < n ? g[c] : 0.0f;
+    bs[c] = c < n ? b[c] : 0.0f;
   }
+  __syncthreads();
   float mx = 0.0f;
   int bad = 0;
   for (int r = r0 + warp; r < r1; r += nw) {
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(1024)
     for (int i = 0; i < KPL; ++i) {
       const int c = lane + 32 * i;
       if (c < n) {
-        const float v = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[i], mu), inv), gv[i]), bv[i]);
+        const float v = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[i], mu), inv), gs[c]), bs[c]);
         yr[c] = v;
         if (staged) ysm[(r - r0) * n + c] = v;
         mx = fmaxf(mx, fabsf(v));
