@@ -926,9 +926,9 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
   const OperandOut od = opout(act_d_), off_ = opout(act_ff_);
   for (int l = 0; l < c.num_encoder_layers; ++l) {
     EncLayer& L = enc_[l];
-    enc_ln_tr_ = enc_trace(l, 5, "enc layernorm 1");
+    enc_ln_tr_ = enc_trace(l, 0, "enc layernorm 1");
     ln_enc(enc_x_.get(), m, L.n1, enc_a_.get(), act_d_);
-    cur_tr_ = enc_trace(l, 0, "enc gemm qkv");
+    cur_tr_ = enc_trace(l, 1, "enc gemm qkv");
     gemm(act_d_, L.qkv, m, nullptr, enc_qkv_.get(), 3 * d, nullptr, nullptr, 0);
     const bool plain = prec_is_tf32x3(act_d_.prec);  // fp32: contexts are the operand
     // bf16 (head dim 64, unpadded rows): the attention writes the bf16
@@ -942,7 +942,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
                          heads_, scale, ctx_out, plain || bf16_direct ? act_d_.k_pad : d,
                          act_d_.prec == kPrecTF32x3 ? act_d_.lo.get() : nullptr,
                          fused ? sent_absmax_.get() : nullptr, nonfinite_.get(), stream_,
-                         enc_trace(l, 1, "enc attention"), bf16_direct);
+                         enc_trace(l, 2, "enc attention"), bf16_direct);
     count("enc attention");
     if (plain || bf16_direct) {
     } else if (fused) {
@@ -952,11 +952,11 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     } else {
       prep_enc(enc_ctx_.get(), d, d_, m, act_d_, false);
     }
-    cur_tr_ = enc_trace(l, 2, "enc gemm wo (+res)");
+    cur_tr_ = enc_trace(l, 3, "enc gemm wo (+res)");
     gemm(act_d_, L.wo, m, nullptr, enc_x_.get(), d, nullptr, enc_x_.get(), 0);
-    enc_ln_tr_ = enc_trace(l, 6, "enc layernorm 2");
+    enc_ln_tr_ = enc_trace(l, 4, "enc layernorm 2");
     ln_enc(enc_x_.get(), m, L.n2, enc_a_.get(), act_d_);
-    cur_tr_ = enc_trace(l, 3, "enc gemm w1 (+b1, relu)");
+    cur_tr_ = enc_trace(l, 5, "enc gemm w1 (+b1, relu)");
     if (plain) {
       gemm(act_d_, L.w1, m, nullptr, act_ff_.hi.get(), act_ff_.k_pad, L.b1.get(), nullptr, 1, 0,
            nullptr, nullptr, act_ff_.prec == kPrecTF32x3 ? act_ff_.lo.get() : nullptr);
@@ -975,7 +975,7 @@ void Engine::run_encoder_body(int n_sent, int m, int max_src) {
     } else {
       prep_enc(ffh_.get(), dff_, dff_, m, act_ff_, false);
     }
-    cur_tr_ = enc_trace(l, 4, "enc gemm w2 (+b2, res)");
+    cur_tr_ = enc_trace(l, 6, "enc gemm w2 (+b2, res)");
     gemm(act_ff_, L.w2, m, nullptr, enc_x_.get(), d, L.b2.get(), enc_x_.get(), 0);
   }
   if (c.num_decoder_layers == 0) {
@@ -1173,6 +1173,8 @@ std::string Engine::trace_report() {
     int nl = 0;
     long long prev_end = -1;
     long long layer_first = -1, prev_layer_first = -1;
+    int first_slot = 0;  // first traced slot of a layer (the LayerNorm only for int8)
+    while (first_slot < K && (e[2 * first_slot] == ~0ull || e[2 * first_slot + 1] == 0ull)) ++first_slot;
     for (int l = 0; l < L; ++l) {
       for (int k = 0; k < K; ++k) {
         const unsigned long long b0 = e[2 * (size_t(l) * K + k)], b1 = e[2 * (size_t(l) * K + k) + 1];
@@ -1183,7 +1185,7 @@ std::string Engine::trace_report() {
           g[k] += double(b0) - double(prev_end);
           ++ng[k];
         }
-        if (k == 0) {
+        if (k == first_slot) {
           prev_layer_first = layer_first;
           layer_first = static_cast<long long>(b0);
           if (prev_layer_first >= 0) {
