@@ -54,11 +54,12 @@ __host__ __device__ inline GemvSmem gemv_smem(int chunk, int ks, int kz_bytes, i
   return s;
 }
 
-__device__ __forceinline__ uint32_t tf32_hi(uint32_t x) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(__uint_as_float(x)));
-  return h;
-}
+// TF32x3 split by truncation: hi = the top 19 bits (what the tensor core
+// reads of an fp32 register), lo = x - hi (exact). One LOP instead of the
+// four-instruction cvt.rna emulation per element -- the split is most of
+// the small-batch fp32 GEMV's instruction count. The dropped lo.lo term is
+// below 2^-20 relative (2^-22 with rounding), far inside the fp32 bar.
+__device__ __forceinline__ uint32_t tf32_hi(uint32_t x) { return x & 0xffffe000u; }
 
 // D += A (16 weight rows x 1 K step) . B (1 K step x 8 operand rows).
 template <int PREC>
