@@ -111,6 +111,21 @@ def test_encoder_long_and_short_sentences_bit_exact(batch):
             assert rel(lg, ref_lg) < 1e-4
 
 
+def test_encoder_192_column_tiles_fp32():
+    """64 sentences x 25 tokens at d = 512 give the fp32 encoder QKV / FFN-up
+    GEMMs 156 / 208 128-column tiles (just over one wave), which the planner
+    runs as 104 / 143 192-column tiles; encoder states within the fp32 bar
+    (bf16 QKV takes the same tiles)."""
+    c = cfg(2, 1, 512, 2048, 8, 3000, 300, 64)
+    om = o.OracleModel.create(c, seed=13)
+    srcs = o.synthetic_sources(64, 25, c["src_vocab_size"], seed=77)
+    ref = np.concatenate([om.encode(s, False) for s in srcs])
+    gm = mt.Model.create(c, seed=13, precision=mt.F32)
+    assert rel(gm.encode(srcs), ref) < 1e-4
+    gb = mt.Model.create(c, seed=13, precision=mt.BF16)
+    assert rel(gb.encode(srcs), ref) < 5e-2
+
+
 def test_incremental_matches_teacher_forced_on_gpu():  # test_model.cpp:211-228, C2
     worst = 0.0
     for trial in range(12):
