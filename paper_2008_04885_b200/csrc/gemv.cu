@@ -23,6 +23,17 @@ namespace {
 
 constexpr int kGemvThreads = 256;
 constexpr int kGemvWarps = kGemvThreads / 32;
+// The output projection adds kEpiWarps epilogue warps: chunk i's logits /
+// softmax partials overlap chunk i + 1's MMAs (named barriers, partials
+// double-buffered).
+constexpr int kEpiWarps = 8;
+constexpr int kLogitsThreads = kGemvThreads + 32 * kEpiWarps;
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 constexpr int kMaxGemvStages = 4;
 constexpr int kLnKpl = 16;       // LayerNorm rows of d <= 512 in registers
 constexpr int kKStepBytes = 32;  // one mma K step: 32 int8 / 16 bf16 / 8 tf32 elements
@@ -47,9 +58,11 @@ __host__ __device__ inline GemvSmem gemv_smem(int chunk, int ks, int kz_bytes, i
   s.nst = nst;
   s.a_off = nst * s.stage_bytes;
   s.part_off = s.a_off + kGemvRows * (kz_bytes + 16);
-  s.scale_off = s.part_off + ks * kGemvRows * chunk * 4;
+  // the projection double-buffers the partials: a chunk's epilogue overlaps
+  // the next chunk's MMAs (no CTA barrier between them)
+  s.scale_off = s.part_off + (logits ? 2 : 1) * ks * kGemvRows * chunk * 4;
   s.ex_off = s.scale_off + kGemvRows * 4 * 4;  // [rows][4 segments] int8 epilogue factors
-  s.bar_off = (s.ex_off + (logits ? kGemvWarps * kGemvRows * 33 * 4 : 0) + 7) / 8 * 8;
+  s.bar_off = (s.ex_off + (logits ? kEpiWarps * kGemvRows * 33 * 4 : 0) + 7) / 8 * 8;
   s.total = s.bar_off + kMaxGemvStages * 8 + 8;
   return s;
 }
@@ -181,7 +194,7 @@ __device__ __forceinline__ void store_vec4(uint8_t* A, int P, int n, int c, floa
 // through `ws`; the last CTA of a chunk (ticket `sem`) adds them in split
 // order and runs the epilogue.
 template <int PREC, bool LOGITS, int kRowV4>
-__global__ void __launch_bounds__(kGemvThreads, 1)
+__global__ void __launch_bounds__(LOGITS ? kLogitsThreads : kGemvThreads, 1)
     gemv_kernel(const GemvArgs a, int chunk, int ks, int nst, uint32_t piece) {
   constexpr int E = GemvElem<PREC>::bytes;
   extern __shared__ __align__(128) uint8_t sm[];
@@ -193,7 +206,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   uint8_t* stages = sm;
   uint8_t* A = sm + L.a_off;
   const int AP = kz_bytes + 16;  // operand row pitch (bytes)
-  uint32_t* part = reinterpret_cast<uint32_t*>(sm + L.part_off);
+  uint32_t* const part_base = reinterpret_cast<uint32_t*>(sm + L.part_off);
   float* inv = reinterpret_cast<float*>(sm + L.scale_off);  // [r][seg] (int8)
   float* ex = reinterpret_cast<float*>(sm + L.ex_off);      // [warp][row][33] (projection)
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.bar_off);
@@ -324,7 +337,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   // ---- operand row r = warp (rows past the allocation are zero) ----
   // int8: one scale per row (each hypothesis row is one quantize call,
   // quant.cpp:108-122).
-  {
+  if (r < kGemvRows) {
     int bad = 0;
     float scale = 1.0f;
     uint8_t* arow = A + r * AP;
@@ -393,48 +406,64 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   const int s_begin = kr * kz_steps / ks, s_end = (kr + 1) * kz_steps / ks;
   const int g = lane >> 2, q = lane & 3;
   const long long step_off = a.c_step_stride ? static_cast<long long>(t) * a.c_step_stride : 0LL;
+  const bool mma_warp = warp < kGemvWarps;  // projection: warps >= 8 run the epilogues
   for (int i = 0; i < my_count; ++i) {
     const int s = i % nst;
-    mbar_wait(&full[s], (i / nst) & 1);
-    if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 3);  // weights landed
-    if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 6);  // last chunk landed
+    // Projection: partial buffer b = i & 1, barriers ready[b] (id 1 + b: MMA
+    // warps arrive, epilogue warps wait) and free[b] (id 3 + b: epilogue
+    // warps arrive after chunk i, MMA warps wait before chunk i + 2).
+    const int b = i & 1;
+    uint32_t* const part = part_base + (LOGITS ? b * ks * kGemvRows * chunk : 0);
     const int cidx = blockIdx.x + i * G;
     const int n0 = cidx * chunk;
     const int ncols = min(chunk, a.N - n0);
-    if (gi * 16 < chunk) {
-      // group gi of the chunk: [K step][lane][16 bytes]
-      const uint8_t* wf = stages + s * L.stage_bytes + gi * kz_steps * 512 + lane * 16;
-      const uint8_t* xf = A + g * AP + 4 * q;  // operand row g, the lane's K bytes
-      uint32_t d[4] = {0u, 0u, 0u, 0u};
-      if constexpr (PREC == 2) {
-        uint32_t d1[4] = {0u, 0u, 0u, 0u}, d2[4] = {0u, 0u, 0u, 0u};
-#pragma unroll 4
-        for (int st = s_begin; st < s_end; ++st)
-          mma_step_tf32x3(d1, d2, d, wf + st * 512, xf + st * kKStepBytes);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          d[e] = __float_as_uint(__fadd_rn(
-              __fadd_rn(__uint_as_float(d1[e]), __uint_as_float(d2[e])), __uint_as_float(d[e])));
-      } else {
-#pragma unroll 4
-        for (int st = s_begin; st < s_end; ++st) mma_step<PREC>(d, wf + st * 512, xf + st * kKStepBytes);
+    if (mma_warp) {
+      if constexpr (LOGITS) {
+        if (i >= 2) named_sync(3 + b, kLogitsThreads);
       }
-      uint32_t* pp = part + kr * kGemvRows * chunk;
-      const int c0 = gi * 16 + g;
-      pp[(2 * q) * chunk + c0] = d[0];
-      pp[(2 * q + 1) * chunk + c0] = d[1];
-      pp[(2 * q) * chunk + c0 + 8] = d[2];
-      pp[(2 * q + 1) * chunk + c0 + 8] = d[3];
+      mbar_wait(&full[s], (i / nst) & 1);
+      if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 3);  // weights landed
+      if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 6);  // last chunk landed
+      if (gi * 16 < chunk) {
+        // group gi of the chunk: [K step][lane][16 bytes]
+        const uint8_t* wf = stages + s * L.stage_bytes + gi * kz_steps * 512 + lane * 16;
+        const uint8_t* xf = A + g * AP + 4 * q;  // operand row g, the lane's K bytes
+        uint32_t d[4] = {0u, 0u, 0u, 0u};
+        if constexpr (PREC == 2) {
+          uint32_t d1[4] = {0u, 0u, 0u, 0u}, d2[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 4
+          for (int st = s_begin; st < s_end; ++st)
+            mma_step_tf32x3(d1, d2, d, wf + st * 512, xf + st * kKStepBytes);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            d[e] = __float_as_uint(__fadd_rn(
+                __fadd_rn(__uint_as_float(d1[e]), __uint_as_float(d2[e])), __uint_as_float(d[e])));
+        } else {
+#pragma unroll 4
+          for (int st = s_begin; st < s_end; ++st) mma_step<PREC>(d, wf + st * 512, xf + st * kKStepBytes);
+        }
+        uint32_t* pp = part + kr * kGemvRows * chunk;
+        const int c0 = gi * 16 + g;
+        pp[(2 * q) * chunk + c0] = d[0];
+        pp[(2 * q + 1) * chunk + c0] = d[1];
+        pp[(2 * q) * chunk + c0 + 8] = d[2];
+        pp[(2 * q + 1) * chunk + c0 + 8] = d[3];
+      }
+      if constexpr (LOGITS) {
+        named_arrive(1 + b, kLogitsThreads);  // partials complete
+        named_sync(5, kGemvThreads);          // stage s consumed
+      } else {
+        __syncthreads();  // stage s consumed, partials complete
+      }
+      if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 4);  // first chunk's MMAs done
+      if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 7);  // last chunk's MMAs done
+      if (warp == 0 && i + nst < my_count) issue(i + nst);
     }
-    __syncthreads();  // stage s consumed, partials complete
-    if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 4);  // first chunk's MMAs done
-    if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 7);  // last chunk's MMAs done
-    if (warp == 0 && i + nst < my_count) issue(i + nst);
 
     // Split-K: publish this CTA's sums; the chunk's last CTA adds all splits
     // in split order (deterministic) and runs the epilogue.
     bool last = true;
-    if (nz > 1) {
+    if (!LOGITS && nz > 1) {
       float* wsc = a.ws + static_cast<long long>(cidx) * nz * kGemvRows * chunk;
       for (int idx = threadIdx.x; idx < R * chunk; idx += blockDim.x) {
         const int rr = idx / chunk, c = idx - rr * chunk;
@@ -511,17 +540,19 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           a.C[step_off + rr * a.ldc + n] = y;
         }
       }
-    } else {
+    } else if (!mma_warp) {
+      named_sync(1 + b, kLogitsThreads);  // chunk i's partials
       // Output projection: warps take (32-column slice, block of RB rows)
       // items and store the logits of those rows and the slice partials --
       // max, first argmax (strict >, so NaN never wins) and the sum of
       // exp(x - max) in column order (P6). The exps are lane-parallel; the
       // ordered sums run one row per lane.
       const int n_sl = (ncols + 31) / 32;
-      const int RB = max(1, (R * n_sl + kGemvWarps - 1) / kGemvWarps);
+      const int ew = warp - kGemvWarps;
+      const int RB = max(1, (R * n_sl + kEpiWarps - 1) / kEpiWarps);
       const int nrb = (R + RB - 1) / RB;
-      float* e = ex + warp * (kGemvRows * 33);
-      for (int it = warp; it < n_sl * nrb; it += kGemvWarps) {
+      float* e = ex + ew * (kGemvRows * 33);
+      for (int it = ew; it < n_sl * nrb; it += kEpiWarps) {
         const int sl = it / nrb, r0 = (it - sl * nrb) * RB, r1 = min(R, r0 + RB);
         const int c = sl * 32 + lane;
         const int nv = min(32, ncols - sl * 32);
@@ -572,9 +603,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         }
         __syncwarp();
       }
+      if (i + 2 < my_count) named_arrive(3 + b, kLogitsThreads);  // buffer b free
     }
-    __syncthreads();  // partials reused by the next chunk
+    if constexpr (!LOGITS) __syncthreads();  // partials reused by the next chunk
   }
+  if (LOGITS && a.trace.buf) __syncthreads();  // the exit time includes the epilogue warps
   if (threadIdx.x == 0) trace_phase(a.trace, 5);
   trace_end(a.trace);
 }
@@ -623,7 +656,8 @@ void launch_gemv_t(const GemvArgs& a, cudaStream_t st) {
     const long v = e ? std::atol(e) : 1L << 20;  // measured: one copy per group is fastest
     return static_cast<uint32_t>(std::max<long>(16, v / 16 * 16));
   }();
-  launch_k(k, dim3(grid, nz), kGemvThreads, L.total, st, a, chunk, ks, nst, piece);
+  launch_k(k, dim3(grid, nz), LOGITS ? kLogitsThreads : kGemvThreads, L.total, st, a, chunk, ks, nst,
+           piece);
   MTG_CUDA(cudaGetLastError());
 }
 
