@@ -172,12 +172,10 @@ template <int PREC>
 __device__ __forceinline__ void store_vec4(uint8_t* A, int P, int n, int c, float4 v, float scale) {
   constexpr int E = GemvElem<PREC>::bytes;
   uint8_t* p = A + n * P + c * E;
-  if constexpr (PREC == 0) {
-    const uint32_t w = (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v.x, scale)))) |
-                       (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v.y, scale))) << 8) |
-                       (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v.z, scale))) << 16) |
-                       (static_cast<uint32_t>(static_cast<uint8_t>(quant1(v.w, scale))) << 24);
-    *reinterpret_cast<uint32_t*>(p) = w;
+  if constexpr (PREC == 0) {  // scale from the row's own max: in range
+    const uint32_t lo = __byte_perm(quant1_in_range(v.x, scale), quant1_in_range(v.y, scale), 0x0040);
+    const uint32_t hi = __byte_perm(quant1_in_range(v.z, scale), quant1_in_range(v.w, scale), 0x0040);
+    *reinterpret_cast<uint32_t*>(p) = __byte_perm(lo, hi, 0x5410);
   } else if constexpr (PREC == 1) {
     const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
     *reinterpret_cast<uint2*>(p) =
@@ -351,29 +349,52 @@ __global__ void __launch_bounds__(LOGITS ? kLogitsThreads : kGemvThreads, 1)
           if (lane + 32 * i < a.K) a.x_out[r * a.ldx_out + lane + 32 * i] = v[i];
       }
       const float mx = ln_normalize_regs<kLnKpl>(v, gv, bv, a.K, lane, &bad);
+      if (MTG_TRACE_PHASES == 2 && threadIdx.x == 0) trace_phase(a.trace, 6);
       scale = qscale_of(mx);
+      if (kzn >= 32 * kLnKpl) {
+        // whole register row inside the operand row: unconditional stores
+        // (values past K are 0 and quantize to 0). The per-element guards
+        // compiled to a branch per value and cost ~1 us per int8 GEMV.
 #pragma unroll
-      for (int i = 0; i < kLnKpl; ++i) {
-        const int c = lane + 32 * i;
-        if (c < kzn) store_elem<PREC>(A, AP, r, c, v[i], c < a.K && PREC == 0 ? quant1(v[i], scale) : int8_t(0));
+        for (int i = 0; i < kLnKpl; ++i)
+          store_elem<PREC>(A, AP, r, lane + 32 * i, v[i],
+                           PREC == 0 ? static_cast<int8_t>(quant1_in_range(v[i], scale)) : int8_t(0));
+      } else {
+#pragma unroll
+        for (int i = 0; i < kLnKpl; ++i) {
+          const int c = lane + 32 * i;
+          if (c < kzn) store_elem<PREC>(A, AP, r, c, v[i], c < a.K && PREC == 0 ? quant1(v[i], scale) : int8_t(0));
+        }
       }
       for (int c = 32 * kLnKpl + lane; c < kzn; c += 32) store_elem<PREC>(A, AP, r, c, 0.0f, 0);
+      if (MTG_TRACE_PHASES == 2 && threadIdx.x == 0) trace_phase(a.trace, 7);
     } else if (vec) {
       if constexpr (PREC == 0) {
-        float m = 0.0f;
+        // max |x| and the non-finite test (x * 0 is NaN only for inf / NaN)
+        // as four independent chains
+        float m4[4] = {0.0f, 0.0f, 0.0f, 0.0f}, z4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int i = 0; i < 4 * kRowV4; ++i) {
-          m = fmaxf(m, fabsf(xv[i]));
-          bad |= !isfinite(xv[i]);
+          m4[i & 3] = fmaxf(m4[i & 3], fabsf(xv[i]));
+          z4[i & 3] = __fmaf_rn(xv[i], 0.0f, z4[i & 3]);
         }
-        scale = qscale_of(warp_allmax(m));
+        const float z = __fadd_rn(__fadd_rn(z4[0], z4[1]), __fadd_rn(z4[2], z4[3]));
+        bad = z != z;
+        scale = qscale_of(warp_allmax(fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]))));
       }
+      if (kzn >= 128 * kRowV4) {  // unconditional stores, as above
 #pragma unroll
-      for (int i = 0; i < kRowV4; ++i) {
-        const int c = 4 * lane + 128 * i;
-        if (c >= kzn) break;
-        store_vec4<PREC>(A, AP, r, c, make_float4(xv[4 * i], xv[4 * i + 1], xv[4 * i + 2], xv[4 * i + 3]),
-                         scale);
+        for (int i = 0; i < kRowV4; ++i)
+          store_vec4<PREC>(A, AP, r, 4 * lane + 128 * i,
+                           make_float4(xv[4 * i], xv[4 * i + 1], xv[4 * i + 2], xv[4 * i + 3]), scale);
+      } else {
+#pragma unroll
+        for (int i = 0; i < kRowV4; ++i) {
+          const int c = 4 * lane + 128 * i;
+          if (c >= kzn) break;
+          store_vec4<PREC>(A, AP, r, c, make_float4(xv[4 * i], xv[4 * i + 1], xv[4 * i + 2], xv[4 * i + 3]),
+                           scale);
+        }
       }
     } else {  // plain fp32 rows, generic shapes
       const float* xr = a.x + r * a.ldx;
@@ -423,7 +444,8 @@ __global__ void __launch_bounds__(LOGITS ? kLogitsThreads : kGemvThreads, 1)
       }
       mbar_wait(&full[s], (i / nst) & 1);
       if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 3);  // weights landed
-      if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 6);  // last chunk landed
+      if (MTG_TRACE_PHASES != 2 && threadIdx.x == 0 && i == my_count - 1)
+        trace_phase(a.trace, 6);  // last chunk landed
       if (gi * 16 < chunk) {
         // group gi of the chunk: [K step][lane][16 bytes]
         const uint8_t* wf = stages + s * L.stage_bytes + gi * kz_steps * 512 + lane * 16;
@@ -456,7 +478,8 @@ __global__ void __launch_bounds__(LOGITS ? kLogitsThreads : kGemvThreads, 1)
         __syncthreads();  // stage s consumed, partials complete
       }
       if (threadIdx.x == 0 && i == 0) trace_phase(a.trace, 4);  // first chunk's MMAs done
-      if (threadIdx.x == 0 && i == my_count - 1) trace_phase(a.trace, 7);  // last chunk's MMAs done
+      if (MTG_TRACE_PHASES != 2 && threadIdx.x == 0 && i == my_count - 1)
+        trace_phase(a.trace, 7);  // last chunk's MMAs done
       if (warp == 0 && i + nst < my_count) issue(i + nst);
     }
 

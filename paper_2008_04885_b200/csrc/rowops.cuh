@@ -16,6 +16,15 @@ __device__ __forceinline__ int8_t quant1(float x, float scale) {
   v = fminf(127.0f, fmaxf(-127.0f, v));
   return static_cast<int8_t>(v);
 }
+// quant1 for values whose row max gave the scale (|x * scale| <= 127 up to
+// two roundings, so the clamp never binds): roundf as nvcc lowers it --
+// x + copysign(0.5, x) rounded toward zero, truncated -- without the clamp
+// and the FRND (F2I truncates). Same result for every finite x; a row with a
+// non-finite value is an error either way (quant.cpp:110-112).
+__device__ __forceinline__ int quant1_in_range(float x, float scale) {
+  const float p = __fmul_rn(x, scale);
+  return __float2int_rz(__fadd_rz(p, copysignf(0.5f, p)));
+}
 __device__ __forceinline__ float qscale_of(float max_abs) {
   return max_abs == 0.0f ? 1.0f : __fdiv_rn(127.0f, max_abs);
 }
