@@ -591,13 +591,13 @@ __global__ void __launch_bounds__(LOGITS ? kLogitsThreads : kGemvThreads, 1)
           const float best = warp_allmax(ok && v == v ? v : kNegInfF);
           const unsigned hit = __ballot_sync(0xffffffffu, ok && v == best && best > kNegInfF);
           const int bi = hit ? n0 + sl * 32 + __ffs(hit) - 1 : -1;
-          float mn = ok ? v : __int_as_float(0x7f800000);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
           if (bi >= 0 && ok) {
+            // the fast exp has the same bits on [-86.5, 0] (and NaN); other
+            // lanes take the full one (lane-local choice, no warp minimum)
             const float zz = __fsub_rn(v, best);
-            e[k * 33 + lane] =
-                __fsub_rn(mn, best) >= -86.5f ? det_expf_nonpos_fast(zz) : det_expf_nonpos(zz);
+            float ez = det_expf_nonpos_fast(zz);
+            if (!(zz >= -86.5f)) ez = det_expf_nonpos(zz);
+            e[k * 33 + lane] = ez;
           }
           if (lane == k) {
             my_best = best;
@@ -654,8 +654,13 @@ void launch_gemv_t(const GemvArgs& a, cudaStream_t st) {
   // layers over more SMs); projection: whole 32-column slices per chunk.
   int groups = 1;
   if (LOGITS) {
+    // MTG_GEMV_LOGITS_GROUPS caps the 16-column groups per chunk (A/B)
+    static const int cap = [] {
+      const char* e = std::getenv("MTG_GEMV_LOGITS_GROUPS");
+      return e ? std::max(2, std::atoi(e)) : 8;
+    }();
     groups = 2;
-    while (groups < 8 && 16 * (2 * groups) * kz_bytes <= 64 * 1024) groups *= 2;
+    while (groups < std::min(8, cap) && 16 * (2 * groups) * kz_bytes <= 64 * 1024) groups *= 2;
   }
   const int ks = std::min(kGemvWarps / groups, ksteps);
   const int chunk = 16 * groups;
